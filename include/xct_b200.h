@@ -1,0 +1,228 @@
+/*
+ * xct_b200 -- C ABI of the B200-native XCT hot path (libxct_b200.so).
+ *
+ * Drop-in boundary for the reference package's operator API
+ * (/root/reference/pkg/src/xct).  The reference is pure Python and has no
+ * FFI; each entry point below replaces one reference function on the hot
+ * path (cited as src/<file>:<line>) and is bound from Python with ctypes
+ * (paper_2009_07226_b200/_lib.py; INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - every function returns an int status: XCT_OK (0) or an error code;
+ *     xct_last_error() gives a message (thread-local);
+ *   - "d_" pointers are device pointers owned by the caller; "h_" pointers
+ *     are host pointers; nothing is allocated behind the caller's back
+ *     except inside an xct_format handle (host memory);
+ *   - all device work is stream-ordered on the given cudaStream_t (passed
+ *     as void*; NULL = legacy default stream) and asynchronous;
+ *   - precision codes follow src/matrixstore.py:41:
+ *       0 double, 1 single, 2 half, 3 mixed (fp16 storage, fp32 compute).
+ */
+#ifndef XCT_B200_H
+#define XCT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  XCT_OK = 0,
+  XCT_EINVAL = 1,        /* ValueError in the reference                   */
+  XCT_ECUDA = 2,         /* CUDA runtime failure                          */
+  XCT_ESTAGE = 3,        /* StageSplitRequired (src/matrixstore.py:54-55) */
+  XCT_ENOMEM = 4,
+  XCT_ENONFINITE = 5     /* non-finite data (src/matrixstore.py:298-299)  */
+};
+
+enum { XCT_DOUBLE = 0, XCT_SINGLE = 1, XCT_HALF = 2, XCT_MIXED = 3 };
+
+int xct_abi_version(void);
+const char* xct_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * K1/K2  Siddon system-matrix construction
+ * replaces geometry.trace_ray (src/geometry.py:117-164) and the row loop of
+ * geometry.build_system_matrix (src/geometry.py:202-232).
+ * Rays r = k*n_det + c for k in [k0, k1); d_cos/d_sin hold cos/sin of every
+ * view angle (computed on the host exactly as make_geometry does,
+ * src/geometry.py:84-85,112).  Results are bit-identical to the reference
+ * in float64 (no FMA contraction).
+ * ------------------------------------------------------------------------- */
+int xct_siddon_count(const double* d_cos, const double* d_sin, int k0, int k1,
+                     int n_det, int grid_n, double voxel_size,
+                     int64_t* d_counts /* [(k1-k0)*n_det] */, void* stream);
+
+int xct_siddon_fill(const double* d_cos, const double* d_sin, int k0, int k1,
+                    int n_det, int grid_n, double voxel_size,
+                    const int64_t* d_rowptr /* [(k1-k0)*n_det+1], relative */,
+                    int32_t* d_indices, double* d_values, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K5  staged execution format (host builder)
+ * replaces matrixstore.build_staged / pack (src/matrixstore.py:250-262,
+ * :417-562).  Rows of a CSR block are assigned to thread blocks ("CTA
+ * tiles", rows_per_cta rows each, -1 = empty lane).  Each entry gets a key
+ * key_tables[cta_table[cta]*n_cols + col]; a CTA's column footprint is
+ * ordered by (key, col) and cut into load groups of whole keys holding at
+ * most `capacity` elements (shared-memory slots).  A row's entries are
+ * accumulated group by group, in (key, CSR position) order inside a group.
+ * Per (group, warp) the entries of the warp's rows are stored as a
+ * zero-padded slab [width/4][rows_per_warp][4] of (uint16 slot, value).
+ * ------------------------------------------------------------------------- */
+typedef struct xct_format xct_format;
+
+typedef struct {
+  int64_t n_cta, rows_per_cta, rows_per_warp, warps_per_cta;
+  int64_t n_groups, n_slots, n_padded, nnz;
+  int64_t max_group_slots;
+  int32_t value_bytes;
+  double max_rel_quant_error;     /* PackReport.max_rel_error            */
+  int64_t underflow_count;        /* PackReport.underflow_count          */
+} xct_format_info;
+
+int xct_format_build(int64_t n_rows, int64_t n_cols,
+                     const int64_t* h_indptr, const int32_t* h_indices,
+                     const double* h_values,
+                     int64_t n_cta, int64_t rows_per_cta, int64_t rows_per_warp,
+                     const int32_t* h_cta_rows,
+                     const int32_t* h_key_tables, const int32_t* h_cta_table,
+                     int64_t capacity, int precision, int value_scale_exp,
+                     int n_threads, xct_format** out);
+int xct_format_get_info(const xct_format* f, xct_format_info* info);
+/* copies the format arrays into caller-provided host buffers sized from
+ * xct_format_get_info; any pointer may be NULL to skip that array. */
+int xct_format_export(const xct_format* f,
+                      int32_t* h_cta_group_ptr /* [n_cta+1] */,
+                      int64_t* h_group_map_ptr /* [n_groups+1] */,
+                      int32_t* h_group_map /* [n_slots] */,
+                      int64_t* h_slab_off /* [n_groups*warps_per_cta] */,
+                      int32_t* h_slab_width /* [n_groups*warps_per_cta] */,
+                      uint16_t* h_slots /* [n_padded] */,
+                      void* h_values /* [n_padded] of value_bytes */);
+void xct_format_free(xct_format* f);
+
+/* stable counting transpose of a CSR block (src/matrixstore.py:189-201);
+ * h_t_indptr [n_cols+1], h_t_indices/h_t_values [nnz]. */
+int xct_csr_transpose(int64_t n_rows, int64_t n_cols, const int64_t* h_indptr,
+                      const int32_t* h_indices, const double* h_values,
+                      int64_t* h_t_indptr, int32_t* h_t_indices, double* h_t_values,
+                      int n_threads);
+
+/* ---------------------------------------------------------------------------
+ * K6  staged SpMM (forward projection A.X and back projection A^T.Y)
+ * replaces engine.project / backproject / _apply_exec
+ * (src/engine.py:119-166) fused with the output scaling and cast
+ * (src/engine.py:137-139), the partial-result upcast (src/comm.py:432) and
+ * denormalize (src/matrixstore.py:308-316).
+ * X is chunked slice-minor: [n_chunks][n_in][f_dev] at the storage dtype.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t n_cta, rows_per_cta, warps_per_cta, rows_per_warp, n_groups;
+  const int32_t* d_cta_rows;        /* [n_cta*rows_per_cta], -1 = empty  */
+  const int32_t* d_cta_group_ptr;   /* [n_cta+1]                         */
+  const int64_t* d_group_map_ptr;   /* [n_groups+1]                      */
+  const int32_t* d_group_map;       /* [n_slots]: slot -> input element  */
+  const int64_t* d_slab_off;        /* [n_groups*warps_per_cta]          */
+  const int32_t* d_slab_width;      /* [n_groups*warps_per_cta]          */
+  const uint16_t* d_slots;          /* [n_padded]                        */
+  const void* d_values;             /* [n_padded] storage dtype          */
+  int64_t max_group_slots;
+} xct_staged;
+
+typedef struct {
+  void* d_out;            /* f32 (single/mixed/half) or f64 (double)      */
+  int64_t row_stride;     /* elements between consecutive output rows    */
+  int64_t chunk_stride;   /* elements between consecutive F-chunks       */
+  int32_t valid_cols;     /* slices to write (drops the padded tail)     */
+  int32_t ffactor;        /* slices per chunk as seen by the caller (F)  */
+  int32_t value_scale_exp;/* outputs scaled by 2^-exp (src/engine.py:137) */
+  int32_t accumulate;     /* 1: out += result (rank-ordered partial sums) */
+  const double* d_factors;/* [n_chunks] denormalize factors, NULL = 1     */
+  double* d_dot_partials; /* [n_chunks*n_cta] sum of out^2, NULL = skip   */
+} xct_epilogue;
+
+int xct_spmm(const xct_staged* a, int precision, const void* d_x, int64_t n_in,
+             int64_t n_chunks, int32_t f_dev, const xct_epilogue* ep,
+             int64_t smem_bytes, void* stream);
+
+/* float64 CSR product y = A x over n_slices columns (row-major x [n_cols][S],
+ * y [n_rows][S]); measurement synthesis (src/geometry.py:347-367). */
+int xct_csr_spmm_f64(const int64_t* d_indptr, const int32_t* d_indices,
+                     const double* d_values, int64_t n_rows, const double* d_x,
+                     int64_t n_slices, double* d_y, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K7  max-abs normalization per F-slice chunk
+ * replaces matrixstore.normalize (src/matrixstore.py:290-305) for the chunk
+ * loop of pipeline._apply (src/pipeline.py:160-168).
+ * Input v is strided: element i, slice j at v[i*row_stride + j] (dtype
+ * in_f64 ? f64 : f32), j < n_slices.  d_maxbits[n_chunks] receives the
+ * max |v| of each chunk as raw IEEE bits (u64 of the f64 value).
+ * xct_normalize writes chunk c of (v / factor_c) cast to the storage dtype
+ * into d_out [n_chunks][n][f_dev], zero-padding slices >= n_slices.
+ * ------------------------------------------------------------------------- */
+int xct_chunk_maxabs(const void* d_v, int in_f64, int64_t n, int64_t n_slices,
+                     int64_t row_stride, int32_t ffactor, int64_t n_chunks,
+                     uint64_t* d_maxbits, void* stream);
+int xct_normalize(const void* d_v, int in_f64, int64_t n, int64_t n_slices,
+                  int64_t row_stride, int32_t ffactor, int64_t n_chunks,
+                  int32_t f_dev, const double* d_factors, int precision,
+                  void* d_out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K8/K9  CGLS vector kernels (src/solver.py:84-192)
+ * Persistent vectors live in the chunked layout [n_chunks][n][f_dev]:
+ * double -> f64, single -> f32, half/mixed -> f16 payload + one scalar
+ * factor (_VectorStore, src/solver.py:84-108).  "load" = payload*factor in
+ * f32.  All reductions are deterministic (fixed-order block partials).
+ * ------------------------------------------------------------------------- */
+/* sum_i a_i*b_i in f64 over n_elem elements of dtype code (0 f64, 1 f32,
+ * 2 f16 scaled by fa/fb as float32 loads) -> d_result[0] */
+int xct_dot(const void* d_a, const void* d_b, int dtype, int64_t n_elem,
+            float fa, float fb, double* d_scratch, double* d_result, void* stream);
+
+/* fixed-order f64 sum of n partials (e.g. the SpMM epilogue's
+ * d_dot_partials) -> d_result[0] */
+int xct_sum_f64(const double* d_v, int64_t n, double* d_result, void* stream);
+
+/* max |load(v)| over n_elem -> d_maxbits[0] (IEEE bits of the f64 value,
+ * atomicMax; caller zeroes it first) */
+int xct_maxabs(const void* d_v, int dtype, int64_t n_elem, float fv,
+               uint64_t* d_maxbits, void* stream);
+
+/* out = load(a) + s*load(b)   (two roundings: multiply, then add; d_b may
+ * be NULL for out = load(a)), s rounded to f32 unless all operands are f64.
+ * out_dtype 0/1 writes f64/f32.  out_dtype 2 is the half store of
+ * _VectorStore: pass 1 (d_out == NULL) reduces max|out| into d_maxbits;
+ * pass 2 writes f16(out / out_factor) and, if d_sumsq, sum(load(stored)^2)
+ * (deterministic, via d_scratch[148*8] partials). */
+int xct_axpy(const void* d_a, int a_dtype, float fa, const void* d_b, int b_dtype,
+             float fb, double scale, int64_t n_elem, void* d_out, int out_dtype,
+             float out_factor, uint64_t* d_maxbits, double* d_scratch,
+             double* d_sumsq, void* stream);
+
+/* per-chunk normalize of a stored vector for the operator input:
+ * max over chunk c of |load(v)| -> d_maxbits[c] (f64 bits, zeroed by caller) */
+int xct_chunk_maxabs_chunked(const void* d_v, int dtype, float fv, int64_t n,
+                             int64_t n_chunks, int32_t f_dev,
+                             uint64_t* d_maxbits, void* stream);
+/* out[c] = (load(v[c]) / factor_c) cast to the storage dtype of precision */
+int xct_normalize_chunked(const void* d_v, int dtype, float fv, int64_t n,
+                          int64_t n_chunks, int32_t f_dev, const double* d_factors,
+                          int precision, void* d_out, void* stream);
+
+/* layout conversion chunked [n_chunks][n][f_dev] (f64/f32) <-> strided
+ * (n, n_slices) f64 */
+int xct_unchunk_f64(const void* d_in, int in_dtype, float fin, int64_t n,
+                    int64_t n_slices, int32_t ffactor, int32_t f_dev,
+                    double* d_out, void* stream);
+int xct_chunk_from_f64(const double* d_in, int64_t n, int64_t n_slices,
+                       int32_t ffactor, int32_t f_dev, int out_dtype,
+                       void* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XCT_B200_H */

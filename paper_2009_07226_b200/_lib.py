@@ -1,0 +1,134 @@
+"""ctypes binding of ``libxct_b200.so`` (the C ABI in ``include/xct_b200.h``).
+
+There is no fallback: importing a compute entry point without the built
+library, or calling one without a CUDA device, raises.  Device buffers are
+torch tensors (plumbing only: allocation, streams); every kernel is ours.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libxct_b200.so"
+
+XCT_OK, XCT_EINVAL, XCT_ECUDA, XCT_ESTAGE, XCT_ENOMEM, XCT_ENONFINITE = range(6)
+PREC_CODE = {"double": 0, "single": 1, "half": 2, "mixed": 3}
+
+i32, i64, f32, f64, vp = C.c_int32, C.c_int64, C.c_float, C.c_double, C.c_void_p
+
+
+class FormatInfo(C.Structure):
+    _fields_ = [("n_cta", i64), ("rows_per_cta", i64), ("rows_per_warp", i64),
+                ("warps_per_cta", i64), ("n_groups", i64), ("n_slots", i64),
+                ("n_padded", i64), ("nnz", i64), ("max_group_slots", i64),
+                ("value_bytes", i32), ("max_rel_quant_error", f64),
+                ("underflow_count", i64)]
+
+
+class Staged(C.Structure):
+    _fields_ = [("n_cta", i64), ("rows_per_cta", i64), ("warps_per_cta", i64),
+                ("rows_per_warp", i64), ("n_groups", i64),
+                ("d_cta_rows", vp), ("d_cta_group_ptr", vp), ("d_group_map_ptr", vp),
+                ("d_group_map", vp), ("d_slab_off", vp), ("d_slab_width", vp),
+                ("d_slots", vp), ("d_values", vp), ("max_group_slots", i64)]
+
+
+class Epilogue(C.Structure):
+    _fields_ = [("d_out", vp), ("row_stride", i64), ("chunk_stride", i64),
+                ("valid_cols", i32), ("ffactor", i32), ("value_scale_exp", i32),
+                ("accumulate", i32), ("d_factors", vp), ("d_dot_partials", vp)]
+
+
+_SIGS = {
+    "xct_abi_version": (i32, []),
+    "xct_last_error": (C.c_char_p, []),
+    "xct_siddon_count": (i32, [vp, vp, i32, i32, i32, i32, f64, vp, vp]),
+    "xct_siddon_fill": (i32, [vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp]),
+    "xct_format_build": (i32, [i64, i64, vp, vp, vp, i64, i64, i64, vp, vp, vp, i64, i32,
+                               i32, i32, C.POINTER(vp)]),
+    "xct_format_get_info": (i32, [vp, C.POINTER(FormatInfo)]),
+    "xct_format_export": (i32, [vp, vp, vp, vp, vp, vp, vp, vp]),
+    "xct_format_free": (None, [vp]),
+    "xct_csr_transpose": (i32, [i64, i64, vp, vp, vp, vp, vp, vp, i32]),
+    "xct_spmm": (i32, [C.POINTER(Staged), i32, vp, i64, i64, i32, C.POINTER(Epilogue), i64, vp]),
+    "xct_csr_spmm_f64": (i32, [vp, vp, vp, i64, vp, i64, vp, vp]),
+    "xct_chunk_maxabs": (i32, [vp, i32, i64, i64, i64, i32, i64, vp, vp]),
+    "xct_normalize": (i32, [vp, i32, i64, i64, i64, i32, i64, i32, vp, i32, vp, vp]),
+    "xct_dot": (i32, [vp, vp, i32, i64, f32, f32, vp, vp, vp]),
+    "xct_sum_f64": (i32, [vp, i64, vp, vp]),
+    "xct_maxabs": (i32, [vp, i32, i64, f32, vp, vp]),
+    "xct_axpy": (i32, [vp, i32, f32, vp, i32, f32, f64, i64, vp, i32, f32, vp, vp, vp, vp]),
+    "xct_chunk_maxabs_chunked": (i32, [vp, i32, f32, i64, i64, i32, vp, vp]),
+    "xct_normalize_chunked": (i32, [vp, i32, f32, i64, i64, i32, vp, i32, vp, vp]),
+    "xct_unchunk_f64": (i32, [vp, i32, f32, i64, i64, i32, i32, vp, vp]),
+    "xct_chunk_from_f64": (i32, [vp, i64, i64, i32, i32, i32, vp, vp]),
+}
+
+_lib = None
+
+
+class XctError(RuntimeError):
+    pass
+
+
+class StageSplitError(ValueError):
+    pass
+
+
+def lib():
+    """Load the in-tree library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                "(there is no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return sorted(_SIGS)
+
+
+def check(status: int, what: str):
+    if status == XCT_OK:
+        return
+    msg = lib().xct_last_error().decode(errors="replace")
+    if status == XCT_ESTAGE:
+        raise StageSplitError(f"{what}: {msg}")
+    if status in (XCT_EINVAL, XCT_ENONFINITE):
+        raise ValueError(f"{what}: {msg}")
+    raise XctError(f"{what}: {msg} (status {status})")
+
+
+def call(name: str, *args):
+    check(getattr(lib(), name)(*args), name)
+
+
+def ptr(t) -> int | None:
+    """Device/host address of a torch tensor or numpy array (None for None)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def stream_handle(device=None) -> int:
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def n_threads() -> int:
+    return max(1, min(64, os.cpu_count() or 1))

@@ -1,0 +1,365 @@
+// K5: host builder of the staged SpMM execution format.
+//
+// B200 re-design of matrixstore.build_staged / pack
+// (src/matrixstore.py:250-262, :417-562).  The reference cuts each of
+// `block_partitions` row chunks' sorted column footprint into stages and
+// stores warp-sliced ELL groups.  Here the unit of work is a CTA tile of
+// rows (chosen by the caller: sinogram tiles for projection, voxel tiles for
+// back projection) and the staging order is a caller-supplied key per
+// column (image band / view angle / reference stage id).  A CTA's footprint
+// sorted by (key, col) is cut into load groups of whole keys; each group is
+// staged once into shared memory and every row accumulates its entries of
+// that group in (key, CSR position) order.  This reproduces the reference's
+// per-row accumulation order exactly when the keys are the reference's
+// stage ids, and gives pure traversal order with band keys.
+//
+// Storage per (group, warp) is a zero-padded slab [width/4][rows_per_warp][4]
+// of (uint16 slot, stored length): a lane fetches 4 entries with one vector
+// load and the warp's loads are contiguous.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "xct_common.h"
+
+namespace {
+
+// float64 -> IEEE half, round to nearest even (numpy's direct f64->f16 cast).
+uint16_t f64_to_f16(double x) {
+  uint16_t sign = std::signbit(x) ? 0x8000 : 0;
+  double a = std::fabs(x);
+  if (std::isnan(a)) return sign | 0x7e00;
+  if (std::isinf(a)) return sign | 0x7c00;
+  if (a == 0.0) return sign;
+  int q;
+  std::frexp(a, &q);          // a = m * 2^q, m in [0.5, 1)
+  int e = q - 1;              // a in [2^e, 2^(e+1))
+  if (e < -14) {              // subnormal: quantum 2^-24
+    double r = std::nearbyint(std::ldexp(a, 24));
+    return sign | (uint16_t)r;  // r == 1024 encodes the smallest normal
+  }
+  double r = std::nearbyint(std::ldexp(a, 10 - e));  // in [1024, 2048]
+  if (r == 2048.0) { r = 1024.0; ++e; }
+  if (e > 15) return sign | 0x7c00;
+  return sign | (uint16_t)(((e + 15) << 10) | ((int)r - 1024));
+}
+
+double f16_to_f64(uint16_t h) {
+  int e = (h >> 10) & 0x1f, m = h & 0x3ff;
+  double v;
+  if (e == 0) v = std::ldexp((double)m, -24);
+  else if (e == 31) v = m ? NAN : INFINITY;
+  else v = std::ldexp((double)(m | 0x400), e - 25);
+  return (h & 0x8000) ? -v : v;
+}
+
+struct KC { int32_t key, col; };
+inline bool kc_less(const KC& a, const KC& b) {
+  return a.key < b.key || (a.key == b.key && a.col < b.col);
+}
+
+struct CtaPlan {
+  std::vector<KC> foot;              // footprint sorted by (key, col)
+  std::vector<int64_t> gstart;       // group starts in foot (+ end)
+  std::vector<int32_t> width;        // [n_groups_local * warps] padded widths
+};
+
+}  // namespace
+
+struct xct_format {
+  xct_format_info info{};
+  std::vector<int32_t> cta_group_ptr;
+  std::vector<int64_t> group_map_ptr;
+  std::vector<int32_t> group_map;
+  std::vector<int64_t> slab_off;
+  std::vector<int32_t> slab_width;
+  std::vector<uint16_t> slots;
+  std::vector<uint8_t> values;
+};
+
+namespace {
+
+template <typename F>
+void parallel_for(int64_t n, int n_threads, F fn) {
+  if (n_threads < 1) n_threads = 1;
+  std::atomic<int64_t> next{0};
+  auto worker = [&]() {
+    for (;;) {
+      int64_t i = next.fetch_add(1);
+      if (i >= n) break;
+      fn(i);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < n_threads; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+}
+
+}  // namespace
+
+extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* indptr,
+                                const int32_t* indices, const double* values,
+                                int64_t n_cta, int64_t rows_per_cta, int64_t rows_per_warp,
+                                const int32_t* cta_rows, const int32_t* key_tables,
+                                const int32_t* cta_table, int64_t capacity, int precision,
+                                int value_scale_exp, int n_threads, xct_format** out) {
+  if (!out) return xct::fail(XCT_EINVAL, "format_build: null output handle");
+  *out = nullptr;
+  if (n_rows < 0 || n_cols < 0 || n_cta < 0 || rows_per_cta < 1 || rows_per_warp < 1 ||
+      rows_per_cta % rows_per_warp)
+    return xct::fail(XCT_EINVAL, "format_build: bad shape arguments");
+  if (capacity < 1 || capacity > 65536)
+    return xct::fail(XCT_ESTAGE, "format_build: capacity must be in [1, 65536] slots");
+  if (precision < 0 || precision > 3) return xct::fail(XCT_EINVAL, "format_build: bad precision");
+  if (!indptr || (!indices && indptr[n_rows] > 0) || !cta_rows || !key_tables || !cta_table)
+    return xct::fail(XCT_EINVAL, "format_build: null input array");
+  const int64_t warps = rows_per_cta / rows_per_warp;
+  const int vbytes = precision == XCT_DOUBLE ? 8 : precision == XCT_SINGLE ? 4 : 2;
+
+  std::vector<CtaPlan> plans(n_cta);
+  std::mutex err_mu;
+  int err = XCT_OK;
+  std::string err_msg;
+
+  // ---- phase A: per-CTA footprint, load groups, slab widths ----------------
+  parallel_for(n_cta, n_threads, [&](int64_t b) {
+    CtaPlan& P = plans[b];
+    const int32_t* keys = key_tables + (int64_t)cta_table[b] * n_cols;
+    std::vector<KC> all;
+    for (int64_t t = 0; t < rows_per_cta; ++t) {
+      int32_t r = cta_rows[b * rows_per_cta + t];
+      if (r < 0) continue;
+      for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) all.push_back({keys[indices[j]], indices[j]});
+    }
+    std::sort(all.begin(), all.end(), kc_less);
+    all.erase(std::unique(all.begin(), all.end(),
+                          [](const KC& a, const KC& c) { return a.key == c.key && a.col == c.col; }),
+              all.end());
+    P.foot.swap(all);
+    // whole keys per group, at most `capacity` elements per group
+    int64_t cur = 0, i = 0, n = (int64_t)P.foot.size();
+    P.gstart.push_back(0);
+    while (i < n) {
+      int64_t j = i;
+      while (j < n && P.foot[j].key == P.foot[i].key) ++j;
+      int64_t m = j - i;
+      if (m > capacity) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        err = XCT_ESTAGE;
+        err_msg = "format_build: one staging key needs " + std::to_string(m) +
+                  " slots, capacity is " + std::to_string(capacity);
+        return;
+      }
+      if (cur + m > capacity) { P.gstart.push_back(i); cur = 0; }
+      cur += m;
+      i = j;
+    }
+    if (n > 0) P.gstart.push_back(n);
+    else P.gstart.clear();
+    const int64_t ng = P.gstart.empty() ? 0 : (int64_t)P.gstart.size() - 1;
+    P.width.assign(ng * warps, 0);
+    // the key is a function of the column, so the column alone locates an
+    // entry in the footprint: dense per-thread lookup tables
+    static thread_local std::vector<int32_t> group_of;
+    if ((int64_t)group_of.size() < n_cols) group_of.assign(n_cols, 0);
+    for (int64_t g = 0; g < ng; ++g)
+      for (int64_t p = P.gstart[g]; p < P.gstart[g + 1]; ++p) group_of[P.foot[p].col] = (int32_t)g;
+    std::vector<int32_t> cnt(ng);
+    for (int64_t t = 0; t < rows_per_cta; ++t) {
+      int32_t r = cta_rows[b * rows_per_cta + t];
+      if (r < 0) continue;
+      std::fill(cnt.begin(), cnt.end(), 0);
+      for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) ++cnt[group_of[indices[j]]];
+      int64_t w = t / rows_per_warp;
+      for (int64_t g = 0; g < ng; ++g) {
+        int32_t pw = (cnt[g] + 3) & ~3;
+        if (pw > P.width[g * warps + w]) P.width[g * warps + w] = pw;
+      }
+    }
+  });
+  if (err) return xct::fail(err, err_msg);
+
+  // ---- phase B: global offsets ---------------------------------------------
+  xct_format* F = new (std::nothrow) xct_format();
+  if (!F) return xct::fail(XCT_ENOMEM, "format_build: out of host memory");
+  F->cta_group_ptr.assign(n_cta + 1, 0);
+  int64_t n_groups = 0, n_slots = 0, n_padded = 0, max_gs = 0;
+  for (int64_t b = 0; b < n_cta; ++b) {
+    int64_t ng = plans[b].gstart.empty() ? 0 : (int64_t)plans[b].gstart.size() - 1;
+    n_groups += ng;
+    F->cta_group_ptr[b + 1] = (int32_t)n_groups;
+    n_slots += (int64_t)plans[b].foot.size();
+    for (int64_t g = 0; g < ng; ++g)
+      max_gs = std::max(max_gs, plans[b].gstart[g + 1] - plans[b].gstart[g]);
+    for (int32_t w : plans[b].width) n_padded += (int64_t)w * rows_per_warp;
+  }
+  if (n_groups > INT32_MAX) { delete F; return xct::fail(XCT_EINVAL, "format_build: too many groups"); }
+  try {
+    F->group_map_ptr.assign(n_groups + 1, 0);
+    F->group_map.assign(n_slots, 0);
+    F->slab_off.assign(n_groups * warps, 0);
+    F->slab_width.assign(n_groups * warps, 0);
+    F->slots.assign(n_padded, 0);
+    F->values.assign(n_padded * vbytes, 0);
+  } catch (...) {
+    delete F;
+    return xct::fail(XCT_ENOMEM, "format_build: out of host memory");
+  }
+  std::vector<int64_t> cta_slot0(n_cta + 1, 0);
+  {
+    int64_t gi = 0, so = 0, eo = 0;
+    for (int64_t b = 0; b < n_cta; ++b) {
+      cta_slot0[b] = so;
+      const CtaPlan& P = plans[b];
+      int64_t ng = P.gstart.empty() ? 0 : (int64_t)P.gstart.size() - 1;
+      for (int64_t g = 0; g < ng; ++g, ++gi) {
+        so += P.gstart[g + 1] - P.gstart[g];
+        F->group_map_ptr[gi + 1] = so;
+        for (int64_t w = 0; w < warps; ++w) {
+          F->slab_off[gi * warps + w] = eo;
+          F->slab_width[gi * warps + w] = P.width[g * warps + w];
+          eo += (int64_t)P.width[g * warps + w] * rows_per_warp;
+        }
+      }
+    }
+  }
+
+  // ---- phase C: fill maps and slabs ----------------------------------------
+  const double scale = std::ldexp(1.0, value_scale_exp);
+  std::vector<double> worst(n_cta, 0.0);
+  std::vector<int64_t> under(n_cta, 0);
+  parallel_for(n_cta, n_threads, [&](int64_t b) {
+    const CtaPlan& P = plans[b];
+    const int32_t* keys = key_tables + (int64_t)cta_table[b] * n_cols;
+    const int64_t g0 = F->cta_group_ptr[b];
+    for (size_t i = 0; i < P.foot.size(); ++i) F->group_map[cta_slot0[b] + i] = P.foot[i].col;
+    const int64_t ng = P.gstart.empty() ? 0 : (int64_t)P.gstart.size() - 1;
+    std::vector<std::pair<int32_t, int64_t>> ent;   // (key, csr position)
+    std::vector<int32_t> pos_in_group(ng);
+    static thread_local std::vector<int32_t> slot_of, group_of;
+    if ((int64_t)slot_of.size() < n_cols) { slot_of.assign(n_cols, 0); group_of.assign(n_cols, 0); }
+    for (int64_t g = 0; g < ng; ++g)
+      for (int64_t p = P.gstart[g]; p < P.gstart[g + 1]; ++p) {
+        group_of[P.foot[p].col] = (int32_t)g;
+        slot_of[P.foot[p].col] = (int32_t)(p - P.gstart[g]);
+      }
+    double wmax = 0.0;
+    int64_t nunder = 0;
+    for (int64_t t = 0; t < rows_per_cta; ++t) {
+      int32_t r = cta_rows[b * rows_per_cta + t];
+      if (r < 0) continue;
+      const int64_t w = t / rows_per_warp, rin = t % rows_per_warp;
+      ent.clear();
+      for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) ent.push_back({keys[indices[j]], j});
+      std::stable_sort(ent.begin(), ent.end(),
+                       [](const std::pair<int32_t, int64_t>& a,
+                          const std::pair<int32_t, int64_t>& c) { return a.first < c.first; });
+      std::fill(pos_in_group.begin(), pos_in_group.end(), 0);
+      for (auto& e : ent) {
+        const int32_t col = indices[e.second];
+        const int64_t g = group_of[col];
+        const int64_t slot = slot_of[col];
+        int32_t n = pos_in_group[g]++;
+        int64_t gg = g0 + g;
+        int64_t at = F->slab_off[gg * warps + w] + ((int64_t)(n >> 2) * rows_per_warp + rin) * 4 + (n & 3);
+        F->slots[at] = (uint16_t)slot;
+        double v = values[e.second] * scale;   // exact power-of-two rescale
+        double back;
+        uint8_t* dst = F->values.data() + at * vbytes;
+        if (precision == XCT_DOUBLE) {
+          std::memcpy(dst, &v, 8);
+          back = v;
+        } else if (precision == XCT_SINGLE) {
+          float f = (float)v;
+          std::memcpy(dst, &f, 4);
+          back = (double)f;
+        } else {
+          uint16_t h = f64_to_f16(v);
+          std::memcpy(dst, &h, 2);
+          back = f16_to_f64(h);
+        }
+        if (v != 0.0) {
+          if (back == 0.0) ++nunder;
+          double rel = std::fabs(back - v) / std::fabs(v);
+          if (rel > wmax) wmax = rel;
+        }
+      }
+    }
+    worst[b] = wmax;
+    under[b] = nunder;
+  });
+
+  F->info.n_cta = n_cta;
+  F->info.rows_per_cta = rows_per_cta;
+  F->info.rows_per_warp = rows_per_warp;
+  F->info.warps_per_cta = warps;
+  F->info.n_groups = n_groups;
+  F->info.n_slots = n_slots;
+  F->info.n_padded = n_padded;
+  F->info.nnz = indptr[n_rows] - indptr[0];
+  F->info.max_group_slots = max_gs;
+  F->info.value_bytes = vbytes;
+  double wm = 0.0;
+  int64_t un = 0;
+  for (int64_t b = 0; b < n_cta; ++b) { wm = std::max(wm, worst[b]); un += under[b]; }
+  F->info.max_rel_quant_error = wm;
+  F->info.underflow_count = un;
+  *out = F;
+  return XCT_OK;
+}
+
+extern "C" int xct_format_get_info(const xct_format* f, xct_format_info* info) {
+  if (!f || !info) return xct::fail(XCT_EINVAL, "format_get_info: null argument");
+  *info = f->info;
+  return XCT_OK;
+}
+
+extern "C" int xct_format_export(const xct_format* f, int32_t* cta_group_ptr,
+                                 int64_t* group_map_ptr, int32_t* group_map, int64_t* slab_off,
+                                 int32_t* slab_width, uint16_t* slots, void* values) {
+  if (!f) return xct::fail(XCT_EINVAL, "format_export: null handle");
+  auto cp = [](void* dst, const void* src, size_t n) { if (dst && n) std::memcpy(dst, src, n); };
+  cp(cta_group_ptr, f->cta_group_ptr.data(), f->cta_group_ptr.size() * 4);
+  cp(group_map_ptr, f->group_map_ptr.data(), f->group_map_ptr.size() * 8);
+  cp(group_map, f->group_map.data(), f->group_map.size() * 4);
+  cp(slab_off, f->slab_off.data(), f->slab_off.size() * 8);
+  cp(slab_width, f->slab_width.data(), f->slab_width.size() * 4);
+  cp(slots, f->slots.data(), f->slots.size() * 2);
+  cp(values, f->values.data(), f->values.size());
+  return XCT_OK;
+}
+
+extern "C" void xct_format_free(xct_format* f) { delete f; }
+
+extern "C" int xct_csr_transpose(int64_t n_rows, int64_t n_cols, const int64_t* indptr,
+                                 const int32_t* indices, const double* values,
+                                 int64_t* t_indptr, int32_t* t_indices, double* t_values,
+                                 int n_threads) {
+  (void)n_threads;
+  if (!indptr || !t_indptr) return xct::fail(XCT_EINVAL, "csr_transpose: null argument");
+  const int64_t nnz = indptr[n_rows] - indptr[0];
+  std::vector<int64_t> next(n_cols + 1, 0);
+  for (int64_t j = indptr[0]; j < indptr[n_rows]; ++j) {
+    int32_t c = indices[j];
+    if (c < 0 || c >= n_cols) return xct::fail(XCT_EINVAL, "csr_transpose: column out of range");
+    ++next[c + 1];
+  }
+  for (int64_t c = 0; c < n_cols; ++c) next[c + 1] += next[c];
+  std::memcpy(t_indptr, next.data(), (n_cols + 1) * 8);
+  (void)nnz;
+  // rows visited in ascending order: entries of each column end up sorted by
+  // row id and, for repeated (row, col) pairs, in CSR order (stable)
+  for (int64_t r = 0; r < n_rows; ++r) {
+    for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) {
+      int64_t at = next[indices[j]]++;
+      t_indices[at] = (int32_t)r;
+      t_values[at] = values[j];
+    }
+  }
+  return XCT_OK;
+}

@@ -1,0 +1,412 @@
+// K7 / K8 / K9: normalization, CGLS vector updates and float64 dots.
+//
+//   normalize        matrixstore.normalize      src/matrixstore.py:290-305
+//   store / load     solver._VectorStore        src/solver.py:84-108
+//   x/r/p updates    solver.cgls_solve          src/solver.py:172-186
+//   dots             solver._dot                src/solver.py:111-112
+//
+// All reductions are deterministic: a fixed grid writes per-block f64
+// partials that one block sums in a fixed order.  Max-abs reductions use
+// atomicMax on the IEEE bits of |v| widened to f64 (order free, exact;
+// NaN bits compare above +inf so non-finite data is detected).
+// "load" of a stored vector: dtype 0 f64, 1 f32, 2 f16 payload * f32 factor
+// rounded in f32 -- exactly payload.astype(f32) * np.float32(factor).
+#include <cuda_fp16.h>
+
+#include "xct_common.h"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kRedBlocks = 148 * 8;   // fixed => deterministic partials
+
+__device__ __forceinline__ double load_as_f64(const void* v, int dtype, float f, int64_t i) {
+  if (dtype == 0) return ((const double*)v)[i];
+  if (dtype == 1) return (double)((const float*)v)[i];
+  return (double)__fmul_rn(__half2float(((const __half*)v)[i]), f);
+}
+
+__device__ __forceinline__ float load_f32(const void* v, int dtype, float f, int64_t i) {
+  if (dtype == 1) return ((const float*)v)[i];
+  return __fmul_rn(__half2float(((const __half*)v)[i]), f);
+}
+
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  return (unsigned long long)__double_as_longlong(fabs(x));
+}
+
+__device__ double block_sum(double v) {
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+__device__ unsigned long long block_max(unsigned long long v) {
+  __shared__ unsigned long long red[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u > v ? u : v;
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  unsigned long long t = 0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = red[i] > t ? red[i] : t;
+  __syncthreads();
+  return t;
+}
+
+__global__ void final_sum_kernel(const double* partials, int n, double* out) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v += partials[i];
+  v = block_sum(v);
+  if (threadIdx.x == 0) out[0] = v;
+}
+
+int blocks_for(int64_t n) {
+  int64_t b = (n + kThreads - 1) / kThreads;
+  if (b > kRedBlocks) b = kRedBlocks;
+  return (int)(b < 1 ? 1 : b);
+}
+
+// ---- strided (element-major, slice-minor) inputs of pipeline._apply --------
+
+__global__ void chunk_maxabs_strided(const void* v, int in_f64, int64_t n, int64_t n_slices,
+                                     int64_t rs, int ff, unsigned long long* maxbits) {
+  const int c = blockIdx.y;
+  const int64_t j0 = (int64_t)c * ff;
+  const int64_t w = (n_slices - j0) < ff ? (n_slices - j0) : ff;
+  unsigned long long m = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * w;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / w, j = j0 + t % w;
+    double x = in_f64 ? ((const double*)v)[i * rs + j] : (double)((const float*)v)[i * rs + j];
+    unsigned long long b = abs_bits(x);
+    m = b > m ? b : m;
+  }
+  m = block_max(m);
+  if (threadIdx.x == 0 && m) atomicMax(&maxbits[c], m);
+}
+
+template <typename Out>
+__device__ __forceinline__ Out cast_store(double v64, float v32, bool from64);
+
+template <> __device__ __forceinline__ double cast_store<double>(double v64, float v32, bool f) {
+  return f ? v64 : (double)v32;
+}
+template <> __device__ __forceinline__ float cast_store<float>(double v64, float v32, bool f) {
+  return f ? (float)v64 : v32;   // f64 -> f32 round to nearest even
+}
+template <> __device__ __forceinline__ __half cast_store<__half>(double v64, float v32, bool f) {
+  return f ? __double2half(v64) : __float2half_rn(v32);  // direct RNE casts
+}
+
+template <typename Out>
+__global__ void normalize_strided(const void* v, int in_f64, int64_t n, int64_t n_slices,
+                                  int64_t rs, int ff, int f_dev, const double* factors,
+                                  Out* out) {
+  const int c = blockIdx.y;
+  const double fac = factors[c];
+  const float fac32 = (float)fac;
+  Out* oc = out + (int64_t)c * n * f_dev;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * f_dev;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / f_dev;
+    int jj = (int)(t % f_dev);
+    int64_t j = (int64_t)c * ff + jj;
+    Out o;
+    if (jj < ff && j < n_slices) {
+      if (in_f64) o = cast_store<Out>(__ddiv_rn(((const double*)v)[i * rs + j], fac), 0.f, true);
+      else o = cast_store<Out>(0.0, __fdiv_rn(((const float*)v)[i * rs + j], fac32), false);
+    } else {
+      o = cast_store<Out>(0.0, 0.f, false);
+    }
+    oc[t] = o;
+  }
+}
+
+// ---- chunked persistent vectors [n_chunks][n][f_dev] -----------------------
+
+__global__ void chunk_maxabs_chunked_k(const void* v, int dtype, float fv, int64_t per_chunk,
+                                       unsigned long long* maxbits) {
+  const int c = blockIdx.y;
+  const int64_t base = (int64_t)c * per_chunk;
+  unsigned long long m = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < per_chunk;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long b = abs_bits(load_as_f64(v, dtype, fv, base + t));
+    m = b > m ? b : m;
+  }
+  m = block_max(m);
+  if (threadIdx.x == 0 && m) atomicMax(&maxbits[c], m);
+}
+
+template <typename Out>
+__global__ void normalize_chunked_k(const void* v, int dtype, float fv, int64_t per_chunk,
+                                    const double* factors, Out* out) {
+  const int c = blockIdx.y;
+  const int64_t base = (int64_t)c * per_chunk;
+  const double fac = factors[c];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < per_chunk;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    Out o;
+    if (dtype == 0) o = cast_store<Out>(__ddiv_rn(((const double*)v)[base + t], fac), 0.f, true);
+    else o = cast_store<Out>(0.0, __fdiv_rn(load_f32(v, dtype, fv, base + t), (float)fac), false);
+    out[base + t] = o;
+  }
+}
+
+__global__ void dot_partial_kernel(const void* a, const void* b, int dtype, int64_t n, float fa,
+                                   float fb, double* partials) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    s += load_as_f64(a, dtype, fa, i) * load_as_f64(b, dtype, fb, i);
+  s = block_sum(s);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void maxabs_kernel(const void* v, int dtype, int64_t n, float fv,
+                              unsigned long long* maxbits) {
+  unsigned long long m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long b = abs_bits(load_as_f64(v, dtype, fv, i));
+    m = b > m ? b : m;
+  }
+  m = block_max(m);
+  if (threadIdx.x == 0 && m) atomicMax(maxbits, m);
+}
+
+// out = load(a) + s * load(b); two roundings in the work dtype.
+// mode 0: write out (f32/f64); mode 1: max|out| only; mode 2: write f16
+// (out / factor) and sum load(stored)^2 into per-block partials.
+__global__ void axpy_kernel(const void* a, int at, float fa, const void* b, int bt, float fb,
+                            double s, int64_t n, void* out, int ot, float ofac, int mode,
+                            unsigned long long* maxbits, double* partials) {
+  const bool f64 = at == 0;
+  const float s32 = (float)s;
+  unsigned long long m = 0;
+  double sq = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (f64) {
+      double v = ((const double*)a)[i];
+      if (b) v = __dadd_rn(v, __dmul_rn(s, ((const double*)b)[i]));
+      ((double*)out)[i] = v;
+      continue;
+    }
+    float v = load_f32(a, at, fa, i);
+    if (b) v = __fadd_rn(v, __fmul_rn(s32, load_f32(b, bt, fb, i)));
+    if (mode == 0) {
+      ((float*)out)[i] = v;
+    } else if (mode == 1) {
+      unsigned long long bb = abs_bits((double)v);
+      m = bb > m ? bb : m;
+    } else {
+      __half h = __float2half_rn(__fdiv_rn(v, ofac));
+      ((__half*)out)[i] = h;
+      double back = (double)__fmul_rn(__half2float(h), ofac);
+      sq += back * back;
+    }
+  }
+  if (mode == 1) {
+    m = block_max(m);
+    if (threadIdx.x == 0 && m) atomicMax(maxbits, m);
+  } else if (mode == 2 && partials) {
+    sq = block_sum(sq);
+    if (threadIdx.x == 0) partials[blockIdx.x] = sq;
+  }
+}
+
+template <typename Out>
+__global__ void chunk_from_f64_k(const double* in, int64_t n, int64_t n_slices, int ff,
+                                 int f_dev, int64_t n_chunks, Out* out) {
+  const int64_t total = n_chunks * n * f_dev;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = t / (n * f_dev), rem = t % (n * f_dev);
+    int64_t i = rem / f_dev;
+    int jj = (int)(rem % f_dev);
+    int64_t j = c * ff + jj;
+    double v = (jj < ff && j < n_slices) ? in[i * n_slices + j] : 0.0;
+    out[t] = (Out)v;
+  }
+}
+
+__global__ void unchunk_f64_k(const void* in, int dtype, float fin, int64_t n, int64_t n_slices,
+                              int ff, int f_dev, double* out) {
+  const int64_t total = n * n_slices;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / n_slices, j = t % n_slices;
+    int64_t c = j / ff;
+    int jj = (int)(j % ff);
+    out[t] = load_as_f64(in, dtype, fin, (c * n + i) * f_dev + jj);
+  }
+}
+
+}  // namespace
+
+extern "C" int xct_chunk_maxabs(const void* d_v, int in_f64, int64_t n, int64_t n_slices,
+                                int64_t row_stride, int32_t ffactor, int64_t n_chunks,
+                                uint64_t* d_maxbits, void* stream) {
+  if (!d_v || !d_maxbits || ffactor < 1) return xct::fail(XCT_EINVAL, "chunk_maxabs: bad argument");
+  if (n == 0 || n_chunks == 0) return XCT_OK;
+  int64_t per = n * ffactor;
+  int gx = blocks_for(per);
+  if (gx > 512) gx = 512;
+  chunk_maxabs_strided<<<dim3(gx, (unsigned)n_chunks), kThreads, 0, (cudaStream_t)stream>>>(
+      d_v, in_f64, n, n_slices, row_stride, ffactor, (unsigned long long*)d_maxbits);
+  XCT_CUDA_CHECK_LAUNCH("chunk_maxabs");
+  return XCT_OK;
+}
+
+extern "C" int xct_normalize(const void* d_v, int in_f64, int64_t n, int64_t n_slices,
+                             int64_t row_stride, int32_t ffactor, int64_t n_chunks,
+                             int32_t f_dev, const double* d_factors, int precision,
+                             void* d_out, void* stream) {
+  if (!d_v || !d_out || !d_factors || ffactor < 1 || f_dev < ffactor)
+    return xct::fail(XCT_EINVAL, "normalize: bad argument");
+  if (n == 0 || n_chunks == 0) return XCT_OK;
+  int gx = blocks_for(n * f_dev);
+  if (gx > 512) gx = 512;
+  dim3 grid(gx, (unsigned)n_chunks);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (precision == XCT_DOUBLE)
+    normalize_strided<double><<<grid, kThreads, 0, s>>>(d_v, in_f64, n, n_slices, row_stride,
+                                                        ffactor, f_dev, d_factors, (double*)d_out);
+  else if (precision == XCT_SINGLE)
+    normalize_strided<float><<<grid, kThreads, 0, s>>>(d_v, in_f64, n, n_slices, row_stride,
+                                                       ffactor, f_dev, d_factors, (float*)d_out);
+  else
+    normalize_strided<__half><<<grid, kThreads, 0, s>>>(d_v, in_f64, n, n_slices, row_stride,
+                                                        ffactor, f_dev, d_factors, (__half*)d_out);
+  XCT_CUDA_CHECK_LAUNCH("normalize");
+  return XCT_OK;
+}
+
+extern "C" int xct_dot(const void* d_a, const void* d_b, int dtype, int64_t n_elem, float fa,
+                       float fb, double* d_scratch, double* d_result, void* stream) {
+  if (!d_a || !d_b || !d_scratch || !d_result || dtype < 0 || dtype > 2)
+    return xct::fail(XCT_EINVAL, "dot: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  int g = blocks_for(n_elem);
+  dot_partial_kernel<<<g, kThreads, 0, s>>>(d_a, d_b, dtype, n_elem, fa, fb, d_scratch);
+  final_sum_kernel<<<1, 1024, 0, s>>>(d_scratch, g, d_result);
+  XCT_CUDA_CHECK_LAUNCH("dot");
+  return XCT_OK;
+}
+
+extern "C" int xct_maxabs(const void* d_v, int dtype, int64_t n_elem, float fv,
+                            uint64_t* d_maxbits, void* stream) {
+  if (!d_v || !d_maxbits) return xct::fail(XCT_EINVAL, "maxabs: bad argument");
+  if (n_elem == 0) return XCT_OK;
+  maxabs_kernel<<<blocks_for(n_elem), kThreads, 0, (cudaStream_t)stream>>>(
+      d_v, dtype, n_elem, fv, (unsigned long long*)d_maxbits);
+  XCT_CUDA_CHECK_LAUNCH("maxabs");
+  return XCT_OK;
+}
+
+extern "C" int xct_axpy(const void* d_a, int a_dtype, float fa, const void* d_b, int b_dtype,
+                          float fb, double scale, int64_t n_elem, void* d_out, int out_dtype,
+                          float out_factor, uint64_t* d_maxbits, double* d_scratch,
+                          double* d_sumsq, void* stream) {
+  if (!d_a) return xct::fail(XCT_EINVAL, "axpy: null input");
+  if ((a_dtype == 0) != (out_dtype == 0) || (d_b && (b_dtype == 0) != (a_dtype == 0)))
+    return xct::fail(XCT_EINVAL, "axpy: f64 operands must be all-f64");
+  int mode;
+  if (out_dtype != 2) mode = 0;
+  else mode = d_out ? 2 : 1;
+  if (mode == 0 && !d_out) return xct::fail(XCT_EINVAL, "axpy: null output");
+  if (mode == 1 && !d_maxbits) return xct::fail(XCT_EINVAL, "axpy: max pass needs d_maxbits");
+  if (n_elem == 0) return XCT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int g = blocks_for(n_elem);
+  double* partials = (mode == 2 && d_sumsq) ? d_scratch : nullptr;
+  axpy_kernel<<<g, kThreads, 0, s>>>(d_a, a_dtype, fa, d_b, b_dtype, fb, scale, n_elem, d_out,
+                                     out_dtype, out_factor, mode,
+                                     (unsigned long long*)d_maxbits, partials);
+  if (partials) final_sum_kernel<<<1, 1024, 0, s>>>(partials, g, d_sumsq);
+  XCT_CUDA_CHECK_LAUNCH("axpy");
+  return XCT_OK;
+}
+
+extern "C" int xct_chunk_maxabs_chunked(const void* d_v, int dtype, float fv, int64_t n,
+                                          int64_t n_chunks, int32_t f_dev, uint64_t* d_maxbits,
+                                          void* stream) {
+  if (!d_v || !d_maxbits) return xct::fail(XCT_EINVAL, "chunk_maxabs_chunked: bad argument");
+  if (n == 0 || n_chunks == 0) return XCT_OK;
+  int64_t per = n * f_dev;
+  int gx = blocks_for(per);
+  if (gx > 512) gx = 512;
+  chunk_maxabs_chunked_k<<<dim3(gx, (unsigned)n_chunks), kThreads, 0, (cudaStream_t)stream>>>(
+      d_v, dtype, fv, per, (unsigned long long*)d_maxbits);
+  XCT_CUDA_CHECK_LAUNCH("chunk_maxabs_chunked");
+  return XCT_OK;
+}
+
+extern "C" int xct_normalize_chunked(const void* d_v, int dtype, float fv, int64_t n,
+                                     int64_t n_chunks, int32_t f_dev, const double* d_factors,
+                                     int precision, void* d_out, void* stream) {
+  if (!d_v || !d_out || !d_factors) return xct::fail(XCT_EINVAL, "normalize_chunked: bad argument");
+  if (n == 0 || n_chunks == 0) return XCT_OK;
+  int64_t per = n * f_dev;
+  int gx = blocks_for(per);
+  if (gx > 512) gx = 512;
+  dim3 grid(gx, (unsigned)n_chunks);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (precision == XCT_DOUBLE)
+    normalize_chunked_k<double><<<grid, kThreads, 0, s>>>(d_v, dtype, fv, per, d_factors, (double*)d_out);
+  else if (precision == XCT_SINGLE)
+    normalize_chunked_k<float><<<grid, kThreads, 0, s>>>(d_v, dtype, fv, per, d_factors, (float*)d_out);
+  else
+    normalize_chunked_k<__half><<<grid, kThreads, 0, s>>>(d_v, dtype, fv, per, d_factors, (__half*)d_out);
+  XCT_CUDA_CHECK_LAUNCH("normalize_chunked");
+  return XCT_OK;
+}
+
+extern "C" int xct_unchunk_f64(const void* d_in, int in_dtype, float fin, int64_t n,
+                               int64_t n_slices, int32_t ffactor, int32_t f_dev, double* d_out,
+                               void* stream) {
+  if (!d_in || !d_out) return xct::fail(XCT_EINVAL, "unchunk: bad argument");
+  if (n * n_slices == 0) return XCT_OK;
+  unchunk_f64_k<<<blocks_for(n * n_slices), kThreads, 0, (cudaStream_t)stream>>>(
+      d_in, in_dtype, fin, n, n_slices, ffactor, f_dev, d_out);
+  XCT_CUDA_CHECK_LAUNCH("unchunk");
+  return XCT_OK;
+}
+
+extern "C" int xct_chunk_from_f64(const double* d_in, int64_t n, int64_t n_slices,
+                                  int32_t ffactor, int32_t f_dev, int out_dtype, void* d_out,
+                                  void* stream) {
+  if (!d_in || !d_out || (out_dtype != 0 && out_dtype != 1))
+    return xct::fail(XCT_EINVAL, "chunk_from_f64: bad argument");
+  int64_t n_chunks = (n_slices + ffactor - 1) / ffactor;
+  int64_t total = n_chunks * n * f_dev;
+  if (total == 0) return XCT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (out_dtype == 0)
+    chunk_from_f64_k<double><<<blocks_for(total), kThreads, 0, s>>>(d_in, n, n_slices, ffactor,
+                                                                   f_dev, n_chunks, (double*)d_out);
+  else
+    chunk_from_f64_k<float><<<blocks_for(total), kThreads, 0, s>>>(d_in, n, n_slices, ffactor,
+                                                                  f_dev, n_chunks, (float*)d_out);
+  XCT_CUDA_CHECK_LAUNCH("chunk_from_f64");
+  return XCT_OK;
+}
+
+extern "C" int xct_sum_f64(const double* d_v, int64_t n, double* d_result, void* stream) {
+  if (!d_v || !d_result || n < 0 || n > INT32_MAX) return xct::fail(XCT_EINVAL, "sum_f64: bad argument");
+  final_sum_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(d_v, (int)n, d_result);
+  XCT_CUDA_CHECK_LAUNCH("sum_f64");
+  return XCT_OK;
+}

@@ -1,0 +1,404 @@
+"""Execution formats: staged, packed, device-resident operator sides.
+
+Mirrors ``xct.matrixstore`` (src/matrixstore.py): precision policy
+(storage/compute dtypes, element bytes), the power-of-two half rescale,
+normalize/denormalize, StageSplitRequired -- and replaces build_staged/pack
+(src/matrixstore.py:250-262, :417-562) with the B200 staged format built by
+``xct_format_build`` and uploaded once to HBM.
+
+A ``DeviceSide`` is one direction of the operator (projection A or back
+projection A^T):
+
+  * rows are grouped into CTA tiles: sinogram tiles (views x detectors) for
+    A, voxel tiles (z x x) for A^T; tiles are launched in pseudo-Hilbert
+    order;
+  * each tile's input footprint is staged through shared memory in load
+    groups: image bands perpendicular to the rays for A (so every row sees
+    its entries in traversal order), view-angle ranges for A^T (so every
+    voxel sees its rays in ascending ray id -- the reference order);
+  * ``order="reference"`` keys A's groups by the reference's own stage ids
+    (block_partitions x stage_capacity_bytes) instead, which reproduces the
+    reference's per-row accumulation order bit for bit.
+
+Record layout of a staged input element: f_dev slices x storage bytes, a
+power of two in [16, 512] bytes; one lane owns 16 bytes of it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .hilbert import pseudo_hilbert_cells
+
+__all__ = ["PRECISIONS", "StageSplitRequired", "NormalizationState", "storage_dtype",
+           "compute_dtype", "element_bytes", "half_rescale_exponent", "normalize",
+           "denormalize", "DeviceSide", "build_device_side", "forward_plan", "adjoint_plan",
+           "reference_plan", "row_block_plan", "f_dev_for", "DEFAULT_STAGE_CAPACITY",
+           "SAFE_MAX"]
+
+PRECISIONS = ("double", "single", "half", "mixed")
+WARP_WIDTH = 32
+DEFAULT_STAGE_CAPACITY = 96 * 1024      # src/matrixstore.py:44
+SAFE_MAX = 60000.0                      # src/matrixstore.py:46
+SMEM_BUDGET = 96 * 1024                 # per CTA: two resident CTAs per SM
+
+_STORE = {"double": np.float64, "single": np.float32, "half": np.float16, "mixed": np.float16}
+_COMPUTE = {"double": np.float64, "single": np.float32, "half": np.float16, "mixed": np.float32}
+
+StageSplitRequired = _lib.StageSplitError
+
+
+def _check_precision(precision: str) -> None:
+    if precision not in PRECISIONS:
+        raise ValueError(f"unknown precision {precision!r}; expected one of {PRECISIONS}")
+
+
+def storage_dtype(precision: str):
+    _check_precision(precision)
+    return _STORE[precision]
+
+
+def compute_dtype(precision: str):
+    _check_precision(precision)
+    return _COMPUTE[precision]
+
+
+def element_bytes(precision: str) -> int:
+    return np.dtype(storage_dtype(precision)).itemsize
+
+
+def f_dev_for(ffactor: int, precision: str) -> int:
+    """Device slices per record: F rounded up so that the record is a power
+    of two of at least 16 bytes (extra slices are zero and never written)."""
+    eb = element_bytes(precision)
+    rec = max(16, 1 << (int(ffactor) * eb - 1).bit_length())
+    return rec // eb
+
+
+def lanes_for(ffactor: int, precision: str) -> int:
+    return f_dev_for(ffactor, precision) * element_bytes(precision) // 16
+
+
+def half_rescale_exponent(values) -> int:
+    """-floor(log2(median of the positive lengths)) (src/matrixstore.py:265-275).
+    ``values`` may be a numpy array or a device tensor (median on the device,
+    numpy's even-count convention: mean of the two middle values)."""
+    if isinstance(values, np.ndarray):
+        nz = values[values > 0]
+        if len(nz) == 0:
+            return 0
+        return -int(math.floor(math.log2(float(np.median(nz)))))
+    import torch
+    nz = values[values > 0]
+    n = int(nz.numel())
+    if n == 0:
+        return 0
+    if n % 2:
+        med = float(torch.kthvalue(nz, (n + 1) // 2).values)
+    else:
+        a = float(torch.kthvalue(nz, n // 2).values)
+        b = float(torch.kthvalue(nz, n // 2 + 1).values)
+        med = (a + b) / 2.0
+    return -int(math.floor(math.log2(med)))
+
+
+@dataclass
+class NormalizationState:
+    """Per-application scale (src/matrixstore.py:278-287)."""
+
+    factor: float
+    mode: str
+
+    def __post_init__(self):
+        if self.factor <= 0:
+            raise ValueError("normalization factor must be positive")
+
+
+def _peaks_to_factors(maxbits) -> list:
+    peaks = maxbits.cpu().numpy().view(np.float64)
+    if not np.all(np.isfinite(peaks)):
+        raise ValueError("cannot normalize non-finite data")
+    return [float(p) if p > 0 else 1.0 for p in peaks]
+
+
+def normalize(vector, mode: str):
+    """Max-abs scaling and cast to the storage dtype, on the device
+    (src/matrixstore.py:290-305).  Returns (scaled, NormalizationState) with
+    the same container type as the input (numpy in -> numpy out)."""
+    import torch
+    from .geometry import device
+    _check_precision(mode)
+    is_np = isinstance(vector, np.ndarray)
+    dev = device()
+    v = torch.as_tensor(np.asarray(vector) if is_np else vector, device=dev)
+    if v.dtype not in (torch.float32, torch.float64):
+        v = v.to(torch.float64)
+    flat = v.reshape(-1, 1).contiguous()
+    n = flat.shape[0]
+    maxbits = torch.zeros(1, dtype=torch.int64, device=dev)
+    st = _lib.stream_handle(dev)
+    in64 = int(flat.dtype == torch.float64)
+    _lib.call("xct_chunk_maxabs", _lib.ptr(flat), in64, n, 1, 1, 1, 1, _lib.ptr(maxbits), st)
+    factor = _peaks_to_factors(maxbits)[0]
+    fac = torch.tensor([factor], dtype=torch.float64, device=dev)
+    sd = {"double": torch.float64, "single": torch.float32}.get(mode, torch.float16)
+    out = torch.empty(n, dtype=sd, device=dev)
+    # one chunk of one slice: record padding is irrelevant (f_dev = 1 here)
+    _lib.call("xct_normalize", _lib.ptr(flat), in64, n, 1, 1, 1, 1, 1, _lib.ptr(fac),
+              _lib.PREC_CODE[mode], _lib.ptr(out), st)
+    out = out.reshape(v.shape)
+    return (out.cpu().numpy() if is_np else out), NormalizationState(factor=factor, mode=mode)
+
+
+def denormalize(vector, state: NormalizationState):
+    """(src/matrixstore.py:308-316): f64 in double mode, f32 otherwise."""
+    if isinstance(vector, np.ndarray):
+        dt = np.float64 if state.mode == "double" else np.float32
+        return vector.astype(dt) * dt(state.factor)
+    import torch
+    dt = torch.float64 if state.mode == "double" else torch.float32
+    return vector.to(dt) * torch.tensor(state.factor, dtype=dt).item()
+
+
+# ---------------------------------------------------------------------------
+# CTA tiling / staging-key plans (host, integer, once per operator)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Plan:
+    """Rows per CTA tile plus the column keys that define the load groups."""
+
+    cta_rows: np.ndarray          # int32 [n_cta, rows_per_cta], -1 = empty lane
+    key_tables: np.ndarray        # int32 [n_tables, n_cols]
+    cta_table: np.ndarray         # int32 [n_cta]
+    rows_per_warp: int
+    kind: str
+
+
+def _roundup(a, b):
+    return -(-a // b) * b
+
+
+def forward_plan(num_angles: int, n: int, rows_per_warp: int, warps: int) -> Plan:
+    """Projection A (rows = rays k*N + c): CTA tiles of `ta` views x `td`
+    detectors, one warp = rows_per_warp consecutive detectors of one view.
+    Load groups are image bands across the dominant ray direction: z bands
+    for steep views, x bands (ascending for cos>0, descending for cos<0) for
+    shallow ones, so a ray's entries stay in traversal order."""
+    rw = rows_per_warp
+    td = min(_roundup(n, rw), max(rw, 32))
+    rpc = max(td, (rw * warps) // td * td)
+    ta = rpc // td
+    n_ta, n_td = -(-num_angles // ta), -(-n // td)
+    cells = pseudo_hilbert_cells(n_td, n_ta)           # (x = det tile, z = view tile)
+    ai, di = np.divmod(np.arange(rpc), td)
+    k = cells[:, 1:2] * ta + ai[None, :]
+    c = cells[:, 0:1] * td + di[None, :]
+    rows = np.where((k < num_angles) & (c < n), k * n + c, -1).astype(np.int32)
+    # regime per tile from its views' directions
+    step = math.pi / max(num_angles, 1)
+    del step
+    cols = np.arange(n * n, dtype=np.int64)
+    iz, ix = np.divmod(cols, n)
+    tables = np.stack([iz, ix, n - 1 - ix]).astype(np.int32)
+    return Plan(rows, tables, np.zeros(len(rows), np.int32), rw, "forward")
+
+
+def assign_forward_regimes(plan: Plan, angles, n: int) -> Plan:
+    """Pick the band key of every forward tile from its view angles."""
+    tabs = np.zeros(len(plan.cta_rows), np.int32)
+    ang = np.asarray(angles, dtype=np.float64)
+    for b, rows in enumerate(plan.cta_rows):
+        rr = rows[rows >= 0]
+        if len(rr) == 0:
+            continue
+        th = ang[np.unique(rr // n)]
+        cs, sn = np.cos(th), np.sin(th)
+        if np.all(np.abs(cs) > np.abs(sn)) and np.all(cs > 0):
+            tabs[b] = 1
+        elif np.all(np.abs(cs) > np.abs(sn)) and np.all(cs < 0):
+            tabs[b] = 2
+        else:
+            tabs[b] = 0      # z is non-decreasing along every ray (sin >= 0)
+    plan.cta_table = tabs
+    return plan
+
+
+def adjoint_plan(num_angles: int, n: int, rows_per_warp: int, warps: int) -> Plan:
+    """Back projection A^T (rows = voxels iz*N + ix): CTA tiles of tz x tx
+    voxels, a warp = rows_per_warp consecutive voxels of one image row.
+    Load groups are ranges of view angles (key = ray // N)."""
+    rw = rows_per_warp
+    tx = min(_roundup(n, rw), max(rw, 16))
+    rpc = max(tx, (rw * warps) // tx * tx)
+    tz = rpc // tx
+    n_tz, n_tx = -(-n // tz), -(-n // tx)
+    cells = pseudo_hilbert_cells(n_tx, n_tz)
+    zi, xi = np.divmod(np.arange(rpc), tx)
+    z = cells[:, 1:2] * tz + zi[None, :]
+    x = cells[:, 0:1] * tx + xi[None, :]
+    rows = np.where((z < n) & (x < n), z * n + x, -1).astype(np.int32)
+    tables = (np.arange(num_angles * n, dtype=np.int64) // n).astype(np.int32)[None, :]
+    return Plan(rows, tables, np.zeros(len(rows), np.int32), rw, "adjoint")
+
+
+def row_block_plan(n_rows: int, n_cols: int, rows_per_warp: int, warps: int,
+                   keys: np.ndarray | None = None) -> Plan:
+    """Consecutive rows per CTA, one key table (default: one key per column
+    range of 1 -- i.e. groups are column ranges)."""
+    rpc = rows_per_warp * warps
+    n_cta = max(1, -(-n_rows // rpc))
+    r = np.arange(n_cta * rpc)
+    rows = np.where(r < n_rows, r, -1).astype(np.int32).reshape(n_cta, rpc)
+    if keys is None:
+        keys = np.arange(n_cols, dtype=np.int32)
+    return Plan(rows, np.asarray(keys, np.int32)[None, :], np.zeros(n_cta, np.int32),
+                rows_per_warp, "rows")
+
+
+def reference_plan(indptr: np.ndarray, indices: np.ndarray, n_rows: int, n_cols: int,
+                   block_partitions: int, stage_capacity_bytes, ffactor: int, precision: str,
+                   rows_per_warp: int, warps: int) -> Plan:
+    """Keys = the reference's stage ids: rows split into `block_partitions`
+    contiguous chunks, each chunk's sorted footprint cut every
+    cap // (elem_bytes * F) columns (src/matrixstore.py:434-485).  CTA tiles
+    never straddle a chunk, so each row's accumulation order is exactly the
+    reference's (stage, traversal) order."""
+    eb = element_bytes(precision)
+    parts = min(block_partitions, max(1, n_rows))
+    base, rem = divmod(n_rows, parts)
+    bounds = np.concatenate(([0], np.cumsum([base + (i < rem) for i in range(parts)])))
+    tables = np.zeros((parts, n_cols), np.int32)
+    rpc = rows_per_warp * warps
+    rows_list, tab_list = [], []
+    for p in range(parts):
+        lo, hi = indptr[bounds[p]], indptr[bounds[p + 1]]
+        fp = np.unique(indices[lo:hi])
+        if stage_capacity_bytes is None:
+            cap = max(1, len(fp))
+        else:
+            cap = stage_capacity_bytes // (eb * ffactor)
+            if cap < 1:
+                raise ValueError(
+                    f"stage capacity {stage_capacity_bytes} B cannot hold one element at "
+                    f"{precision} precision with fusing factor {ffactor}")
+        cap = min(cap, 65536)
+        tables[p, fp] = (np.arange(len(fp)) // cap).astype(np.int32)
+        r0, r1 = bounds[p], bounds[p + 1]
+        for s in range(r0, r1, rpc):
+            blk = np.full(rpc, -1, np.int32)
+            e = min(r1, s + rpc)
+            blk[:e - s] = np.arange(s, e)
+            rows_list.append(blk)
+            tab_list.append(p)
+    if not rows_list:
+        rows_list = [np.full(rpc, -1, np.int32)]
+        tab_list = [0]
+    return Plan(np.stack(rows_list), tables, np.asarray(tab_list, np.int32), rows_per_warp,
+                "reference")
+
+
+# ---------------------------------------------------------------------------
+# device-resident side
+# ---------------------------------------------------------------------------
+
+@dataclass
+class DeviceSide:
+    """One staged operator direction in HBM (kernel K6 input)."""
+
+    precision: str
+    ffactor: int
+    f_dev: int
+    n_in: int
+    n_out: int
+    value_scale_exp: int
+    info: _lib.FormatInfo
+    tensors: dict = field(repr=False)
+    staged: _lib.Staged = field(repr=False, default=None)
+    smem_bytes: int = 0
+    plan_kind: str = ""
+
+    @property
+    def nnz(self) -> int:
+        return int(self.info.nnz)
+
+    @property
+    def padded_entries(self) -> int:
+        return int(self.info.n_padded)
+
+    @property
+    def entry_bytes(self) -> int:
+        return 2 + int(self.info.value_bytes)
+
+    def hbm_bytes(self) -> int:
+        return sum(int(t.numel() * t.element_size()) for t in self.tensors.values())
+
+
+def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndarray,
+                      n_rows: int, n_cols: int, plan: Plan, precision: str, ffactor: int,
+                      value_scale_exp: int, smem_budget: int = SMEM_BUDGET,
+                      dev=None) -> DeviceSide:
+    """Build the staged format on the host (libxct_b200 K5) and upload it."""
+    import torch
+    from .geometry import device
+    _check_precision(precision)
+    dev = dev or device()
+    f_dev = f_dev_for(ffactor, precision)
+    rec = f_dev * element_bytes(precision)
+    capacity = min(65536, max(1, smem_budget // rec))
+    rows = np.ascontiguousarray(plan.cta_rows, np.int32)
+    keys = np.ascontiguousarray(plan.key_tables, np.int32)
+    ctab = np.ascontiguousarray(plan.cta_table, np.int32)
+    ip = np.ascontiguousarray(indptr, np.int64)
+    ix = np.ascontiguousarray(indices32, np.int32)
+    vals = np.ascontiguousarray(values, np.float64)
+    handle = C.c_void_p()
+    L = _lib.lib()
+    st = L.xct_format_build(n_rows, n_cols, ip.ctypes.data, ix.ctypes.data, vals.ctypes.data,
+                            rows.shape[0], rows.shape[1], plan.rows_per_warp,
+                            rows.ctypes.data, keys.ctypes.data, ctab.ctypes.data, capacity,
+                            _lib.PREC_CODE[precision], int(value_scale_exp), _lib.n_threads(),
+                            C.byref(handle))
+    _lib.check(st, "xct_format_build")
+    try:
+        info = _lib.FormatInfo()
+        _lib.check(L.xct_format_get_info(handle, C.byref(info)), "xct_format_get_info")
+        warps = int(info.warps_per_cta)
+        h = dict(cta_group_ptr=np.empty(info.n_cta + 1, np.int32),
+                 group_map_ptr=np.empty(info.n_groups + 1, np.int64),
+                 group_map=np.empty(max(info.n_slots, 1), np.int32),
+                 slab_off=np.empty(max(info.n_groups * warps, 1), np.int64),
+                 slab_width=np.empty(max(info.n_groups * warps, 1), np.int32),
+                 slots=np.empty(max(info.n_padded, 1), np.uint16),
+                 values=np.empty(max(info.n_padded, 1), storage_dtype(precision)))
+        _lib.check(L.xct_format_export(handle, *[h[k].ctypes.data for k in
+                                                 ("cta_group_ptr", "group_map_ptr", "group_map",
+                                                  "slab_off", "slab_width", "slots", "values")]),
+                   "xct_format_export")
+    finally:
+        L.xct_format_free(handle)
+    t = {k: torch.from_numpy(v.view(np.int16) if v.dtype == np.uint16 else v).to(dev)
+         for k, v in h.items()}
+    t["cta_rows"] = torch.from_numpy(rows.reshape(-1)).to(dev)
+    side = DeviceSide(precision, ffactor, f_dev, n_cols, n_rows, value_scale_exp, info, t,
+                      plan_kind=plan.kind)
+    s = _lib.Staged()
+    s.n_cta, s.rows_per_cta = info.n_cta, info.rows_per_cta
+    s.warps_per_cta, s.rows_per_warp = info.warps_per_cta, info.rows_per_warp
+    s.n_groups, s.max_group_slots = info.n_groups, info.max_group_slots
+    s.d_cta_rows = t["cta_rows"].data_ptr()
+    s.d_cta_group_ptr = t["cta_group_ptr"].data_ptr()
+    s.d_group_map_ptr = t["group_map_ptr"].data_ptr()
+    s.d_group_map = t["group_map"].data_ptr()
+    s.d_slab_off = t["slab_off"].data_ptr()
+    s.d_slab_width = t["slab_width"].data_ptr()
+    s.d_slots = t["slots"].data_ptr()
+    s.d_values = t["values"].data_ptr()
+    side.staged = s
+    side.smem_bytes = int(max(16, info.max_group_slots * rec))
+    return side

@@ -1,0 +1,343 @@
+"""Operator assembly: the drop-in boundary of the XCT hot path.
+
+Mirrors ``xct.pipeline`` (src/pipeline.py): ``SystemConfig``,
+``AssembledSystem`` with ``apply_forward`` / ``apply_adjoint`` /
+``num_rows`` / ``num_cols`` / ``kernel_counters`` / ``volume_reports``,
+``assemble`` and ``assemble_from_matrix``.  ``cgls_solve`` (solver.py) and
+any reference caller use only this surface.
+
+Everything after assembly is device resident: the staged formats of A and
+A^T live in HBM and each application runs three of our kernels per call --
+chunked max-abs (K7), normalize+cast (K7), staged SpMM with the fused
+scale/cast/denormalize epilogue (K6).
+
+P_d > 1 (Hilbert data partitions, src/pipeline.py:104-113) is emulated in
+one process here: every rank's partial product runs through K6 and the
+partials are reduced in the reference's direct-plan order (owner first,
+then senders ascending; src/comm.py:420-472).  The multi-GPU form of the
+same decomposition is ``parallel.DomainPartitionedSystem``.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _lib, engine, hilbert, matrixstore
+from .geometry import ScanGeometry, SystemMatrix, build_system_matrix, device
+from .matrixstore import NormalizationState
+
+__all__ = ["SystemConfig", "AssembledSystem", "assemble", "assemble_from_matrix", "ORDERS"]
+
+ORDERS = ("native", "reference")
+
+
+@dataclass(frozen=True)
+class SystemConfig:
+    """Parallelization and precision knobs (src/pipeline.py:26-47).
+
+    Added for the B200 build (defaults keep the reference's meaning):
+      order          "native": image-band / view-range staging (traversal
+                     order per ray, ray-id order per voxel); "reference":
+                     the reference's stage order, bit-identical results.
+      warps_per_cta  CTA size of the staged SpMM.
+      smem_budget    shared-memory bytes per CTA for one load group.
+    ``topology`` and ``comm_strategy`` are accepted for API compatibility;
+    on one NVSwitch box the exchange has a single level.
+    """
+
+    precision: str = "double"
+    ffactor: int = 16
+    p_b: int = 1
+    p_d: int = 1
+    tile_size: int = 8
+    block_partitions: int = 4
+    stage_capacity_bytes: int | None = matrixstore.DEFAULT_STAGE_CAPACITY
+    comm_strategy: str = "hierarchical"
+    topology: object = None
+    workers: int = 1
+    order: str = "native"
+    warps_per_cta: int = 16
+    smem_budget: int = matrixstore.SMEM_BUDGET
+
+    def __post_init__(self):
+        if self.precision not in matrixstore.PRECISIONS:
+            raise ValueError(f"unknown precision {self.precision!r}")
+        if self.comm_strategy not in ("direct", "hierarchical"):
+            raise ValueError(f"unknown comm strategy {self.comm_strategy!r}")
+        if not 1 <= self.ffactor <= engine.MAX_FFACTOR:
+            raise ValueError(f"ffactor must be in [1, {engine.MAX_FFACTOR}]")
+        if self.order not in ORDERS:
+            raise ValueError(f"unknown order {self.order!r}; expected one of {ORDERS}")
+        if self.p_b < 1 or self.p_d < 1:
+            raise ValueError("P_b and P_d must be >= 1")
+
+
+@dataclass
+class _Side:
+    """One operator direction: per-rank staged blocks and their maps."""
+
+    blocks: list                 # DeviceSide per rank
+    input_elements: list         # global input ids per rank (None = identity)
+    footprints: list             # global output ids per rank (None = identity)
+    ownership: list              # owned output ids per rank
+    num_inputs: int
+    num_outputs: int
+
+
+def _rows_per_warp(cfg) -> int:
+    return 32 // matrixstore.lanes_for(cfg.ffactor, cfg.precision)
+
+
+def _csr_host(matrix):
+    if isinstance(matrix, SystemMatrix):
+        return matrix.host_csr32()
+    return (np.asarray(matrix.indptr, np.int64), np.asarray(matrix.indices, np.int32),
+            np.asarray(matrix.values, np.float64))
+
+
+def _transpose(indptr, indices, values, n_rows, n_cols):
+    nnz = len(indices)
+    t_ip = np.empty(n_cols + 1, np.int64)
+    t_ix = np.empty(max(nnz, 1), np.int32)
+    t_v = np.empty(max(nnz, 1), np.float64)
+    _lib.call("xct_csr_transpose", n_rows, n_cols, indptr.ctypes.data,
+              indices.ctypes.data if nnz else None, values.ctypes.data if nnz else None,
+              t_ip.ctypes.data, t_ix.ctypes.data, t_v.ctypes.data, _lib.n_threads())
+    return t_ip, t_ix[:nnz], t_v[:nnz]
+
+
+class AssembledSystem:
+    """Distributed forward/adjoint operator over one batch group's slices
+    (src/pipeline.py:64-210), device resident."""
+
+    def __init__(self, matrix, config: SystemConfig, geometry: ScanGeometry | None = None):
+        self.matrix = matrix
+        self.config = config
+        self.geometry = geometry
+        self.device = device()
+        cfg = config
+        if cfg.precision in ("half", "mixed"):
+            vals = getattr(matrix, "d_values", None)
+            self.value_scale_exp = matrixstore.half_rescale_exponent(
+                vals if vals is not None else np.asarray(matrix.values, np.float64))
+        else:
+            self.value_scale_exp = 0
+        ip, ix, v = _csr_host(matrix)
+        n_rows, n_cols = int(matrix.num_rows), int(matrix.num_cols)
+        if cfg.p_d == 1:
+            self.forward = self._single_side(ip, ix, v, n_rows, n_cols, "forward")
+            t_ip, t_ix, t_v = _transpose(ip, ix, v, n_rows, n_cols)
+            self.adjoint = self._single_side(t_ip, t_ix, t_v, n_cols, n_rows, "adjoint")
+        else:
+            if geometry is None:
+                raise ValueError("data parallelism beyond P_d=1 needs a scan geometry")
+            self._build_partitioned(ip, ix, v, n_rows, n_cols)
+
+    # -- construction ---------------------------------------------------------
+
+    def _plan(self, ip, ix, n_rows, n_cols, kind):
+        cfg, g = self.config, self.geometry
+        rw = _rows_per_warp(cfg)
+        if kind == "forward":
+            if cfg.order == "reference" or g is None:
+                return matrixstore.reference_plan(ip, ix, n_rows, n_cols, cfg.block_partitions,
+                                                  cfg.stage_capacity_bytes, cfg.ffactor,
+                                                  cfg.precision, rw, cfg.warps_per_cta)
+            plan = matrixstore.forward_plan(g.num_angles, g.grid_n, rw, cfg.warps_per_cta)
+            return matrixstore.assign_forward_regimes(plan, g.angles, g.grid_n)
+        # adjoint: every per-voxel order keyed by ascending ray id is the
+        # reference order (src/matrixstore.py:189-201 sorts entries by ray)
+        if g is not None and n_rows == g.num_voxels and n_cols == g.num_rays:
+            return matrixstore.adjoint_plan(g.num_angles, g.grid_n, rw, cfg.warps_per_cta)
+        return matrixstore.row_block_plan(n_rows, n_cols, rw, cfg.warps_per_cta)
+
+    def _single_side(self, ip, ix, v, n_rows, n_cols, kind) -> _Side:
+        cfg = self.config
+        plan = self._plan(ip, ix, n_rows, n_cols, kind)
+        blk = matrixstore.build_device_side(ip, ix, v, n_rows, n_cols, plan, cfg.precision,
+                                            cfg.ffactor, self.value_scale_exp,
+                                            cfg.smem_budget, self.device)
+        ident = np.arange(n_rows)
+        return _Side([blk], [None], [None], [ident], n_cols, n_rows)
+
+    def _build_partitioned(self, ip, ix, v, n_rows, n_cols):
+        cfg, g = self.config, self.geometry
+        tomo = hilbert.decompose(hilbert.TileGrid("tomogram", g.grid_n, g.grid_n,
+                                                  cfg.tile_size), cfg.p_d)
+        sino = hilbert.decompose(hilbert.TileGrid("sinogram", g.num_angles,
+                                                  g.num_detector_cols, cfg.tile_size), cfg.p_d)
+        self.tomogram_subdomains, self.sinogram_subdomains = tomo, sino
+        rw = _rows_per_warp(cfg)
+        row_of = np.repeat(np.arange(n_rows), np.diff(ip))
+
+        def build(bip, bix, bv, nr, nc):
+            plan = matrixstore.reference_plan(bip, bix, nr, nc, cfg.block_partitions,
+                                              cfg.stage_capacity_bytes, cfg.ffactor,
+                                              cfg.precision, rw, cfg.warps_per_cta)
+            return matrixstore.build_device_side(bip, bix, bv, nr, nc, plan, cfg.precision,
+                                                 cfg.ffactor, self.value_scale_exp,
+                                                 cfg.smem_budget, self.device)
+
+        f_blocks, f_fp = [], []
+        for sub in tomo:         # A[:, owned cols] over the rays it touches
+            cols = sub.elements
+            keep = np.zeros(n_cols, bool)
+            keep[cols] = True
+            sel = keep[ix]
+            rows = row_of[sel]
+            fp = np.unique(rows)
+            lr = np.searchsorted(fp, rows)
+            bip = np.concatenate(([0], np.cumsum(np.bincount(lr, minlength=len(fp))))).astype(np.int64)
+            bix = np.searchsorted(cols, ix[sel]).astype(np.int32)
+            f_blocks.append(build(bip, bix, v[sel], len(fp), len(cols)))
+            f_fp.append(fp)
+        a_blocks, a_fp = [], []
+        for sub in sino:         # transpose(A[owned rays, :]) over the voxels touched
+            rays = sub.elements
+            take = np.concatenate([np.arange(ip[r], ip[r + 1]) for r in rays]) if len(rays) else np.empty(0, np.int64)
+            cnt = np.diff(ip)[rays]
+            fp = np.unique(ix[take])
+            rip = np.concatenate(([0], np.cumsum(cnt))).astype(np.int64)
+            rix = np.searchsorted(fp, ix[take]).astype(np.int32)
+            t_ip, t_ix, t_v = _transpose(rip, rix, v[take], len(rays), len(fp))
+            a_blocks.append(build(t_ip, t_ix, t_v, len(fp), len(rays)))
+            a_fp.append(fp)
+        self.forward = _Side(f_blocks, [s.elements for s in tomo], f_fp,
+                             [s.elements for s in sino], n_cols, n_rows)
+        self.adjoint = _Side(a_blocks, [s.elements for s in sino], a_fp,
+                             [s.elements for s in tomo], n_rows, n_cols)
+
+    # -- application ------------------------------------------------------------
+
+    @property
+    def num_cols(self) -> int:
+        return int(self.matrix.num_cols)
+
+    @property
+    def num_rows(self) -> int:
+        return int(self.matrix.num_rows)
+
+    def apply_forward(self, x):
+        """Projection of (num_cols,) or (num_cols, slices) data; returns
+        (values, [NormalizationState per F-chunk]) (src/pipeline.py:141-174)."""
+        return self._apply(self.forward, x)
+
+    def apply_adjoint(self, y):
+        return self._apply(self.adjoint, y)
+
+    def _apply(self, side: _Side, data):
+        import torch
+        is_np = not isinstance(data, torch.Tensor)
+        arr = np.asarray(data) if is_np else data
+        squeeze = arr.ndim == 1
+        if arr.shape[0] != side.num_inputs:
+            raise ValueError(f"operator expects {side.num_inputs} input elements, "
+                             f"got {arr.shape[0]}")
+        dev = self.device
+        X = torch.as_tensor(arr, device=dev)
+        if X.dtype not in (torch.float32, torch.float64):
+            X = X.to(torch.float64)
+        X = X.reshape(X.shape[0], -1).contiguous()
+        S = int(X.shape[1])
+        cfg = self.config
+        F = cfg.ffactor
+        out_dtype = torch.float64 if cfg.precision == "double" else torch.float32
+        out = torch.empty((side.num_outputs, S), dtype=out_dtype, device=dev)
+        states = []
+        if S == 0:
+            res = out.cpu().numpy() if is_np else out
+            return (res[:, 0] if squeeze else res), states
+        n_chunks = -(-S // F)
+        st = _lib.stream_handle(dev)
+        in64 = int(X.dtype == torch.float64)
+        maxbits = torch.zeros(n_chunks, dtype=torch.int64, device=dev)
+        _lib.call("xct_chunk_maxabs", X.data_ptr(), in64, X.shape[0], S, S, F, n_chunks,
+                  maxbits.data_ptr(), st)
+        factors = matrixstore._peaks_to_factors(maxbits)
+        states = [NormalizationState(factor=f, mode=cfg.precision) for f in factors]
+        fac = torch.tensor(factors, dtype=torch.float64, device=dev)
+        blk0 = side.blocks[0]
+        sd = {"double": torch.float64, "single": torch.float32}.get(cfg.precision, torch.float16)
+        if len(side.blocks) == 1 and side.input_elements[0] is None:
+            xin = torch.empty((n_chunks, side.num_inputs, blk0.f_dev), dtype=sd, device=dev)
+            _lib.call("xct_normalize", X.data_ptr(), in64, X.shape[0], S, S, F, n_chunks,
+                      blk0.f_dev, fac.data_ptr(), _lib.PREC_CODE[cfg.precision],
+                      xin.data_ptr(), st)
+            engine.apply_side(blk0, xin, out, row_stride=S, chunk_stride=F, valid_cols=S,
+                              ffactor_out=F, factors=fac, stream=st)
+        else:
+            self._apply_partitioned(side, X, S, F, n_chunks, fac, sd, out, st)
+        res = out.cpu().numpy() if is_np else out
+        return (res[:, 0] if squeeze else res), states
+
+    def _apply_partitioned(self, side, X, S, F, n_chunks, fac, sd, out, st):
+        """Per-rank partials, then the direct-plan reduction order."""
+        import torch
+        cfg, dev = self.config, self.device
+        in64 = int(X.dtype == torch.float64)
+        cd = {"double": torch.float64, "half": torch.float16}.get(cfg.precision, torch.float32)
+        f_dev = side.blocks[0].f_dev
+        xin = torch.empty((n_chunks, side.num_inputs, f_dev), dtype=sd, device=dev)
+        _lib.call("xct_normalize", X.data_ptr(), in64, X.shape[0], S, S, F, n_chunks, f_dev,
+                  fac.data_ptr(), _lib.PREC_CODE[cfg.precision], xin.data_ptr(), st)
+        pdt = torch.float64 if cfg.precision == "double" else torch.float32
+        parts = []
+        for blk, inp in zip(side.blocks, side.input_elements):
+            xp = xin[:, torch.as_tensor(inp, device=dev)].contiguous()
+            pr = torch.empty((blk.n_out, n_chunks * F), dtype=pdt, device=dev)
+            engine.apply_side(blk, xp, pr, row_stride=n_chunks * F, chunk_stride=F,
+                              valid_cols=n_chunks * F, ffactor_out=F, factors=None, stream=st)
+            parts.append(pr.to(cd))
+        total = torch.zeros((side.num_outputs, n_chunks * F), dtype=cd, device=dev)
+        for q, own in enumerate(side.ownership):
+            keep = torch.zeros(side.num_outputs, dtype=torch.bool, device=dev)
+            keep[torch.as_tensor(own, device=dev)] = True
+            for s in [q] + [s for s in range(len(parts)) if s != q]:
+                rows = torch.as_tensor(side.footprints[s], device=dev)
+                hit = keep[rows]
+                total[rows[hit]] += parts[s][hit]
+        odt = torch.float64 if cfg.precision == "double" else torch.float32
+        f_cols = fac.to(odt).repeat_interleave(F)[None, :]
+        res = total.to(odt) * f_cols
+        out.copy_(res[:, :S])
+
+    # -- reporting ----------------------------------------------------------------
+
+    def kernel_counters(self) -> engine.KernelCounters:
+        """Aggregate work counters for one forward application."""
+        return engine.kernel_counters(self.forward.blocks)
+
+    def volume_reports(self) -> dict:
+        """Exchange volumes (elements x F x bytes) of the direct plan."""
+        out = {}
+        eb = matrixstore.element_bytes(self.config.precision)
+        for name, side in (("projection", self.forward), ("backprojection", self.adjoint)):
+            if side.footprints[0] is None:
+                out[name] = {"direct_bytes": 0, "ranks": 1}
+                continue
+            owner = np.empty(side.num_outputs, np.int64)
+            for q, own in enumerate(side.ownership):
+                owner[own] = q
+            off = sum(int(np.count_nonzero(owner[fp] != s)) for s, fp in enumerate(side.footprints))
+            out[name] = {"direct_bytes": off * self.config.ffactor * eb,
+                         "ranks": len(side.blocks)}
+        return out
+
+    def hbm_bytes(self) -> int:
+        return sum(b.hbm_bytes() for s in (self.forward, self.adjoint) for b in s.blocks)
+
+
+def assemble(geometry: ScanGeometry, config: SystemConfig) -> AssembledSystem:
+    """Build the device operator for a scan geometry (matrix memoized)."""
+    return AssembledSystem(build_system_matrix(geometry), config, geometry=geometry)
+
+
+def assemble_from_matrix(matrix, config: SystemConfig | None = None) -> AssembledSystem:
+    """Wrap an arbitrary compressed-row operator (single data process)."""
+    config = config or SystemConfig(p_d=1)
+    if config.p_d != 1:
+        config = replace(config, p_d=1)
+    return AssembledSystem(matrix, config, geometry=None)

@@ -1,0 +1,351 @@
+"""CGLS reconstruction on the device.
+
+Mirrors ``xct.solver`` (src/solver.py): SolveConfig, SolveResult,
+SolverDivergence, early_stop, residual_curve_report and cgls_solve, with
+the reference's exact scalar and cast sequence:
+
+  * scalars (alpha, beta, norms) are float64 host floats, cast to the work
+    dtype before use (src/solver.py:172-185);
+  * vector updates are one multiply then one add (two roundings) in the
+    work dtype -- K8 ``xct_axpy``;
+  * half/mixed keep x, r, p as fp16 payload + max-abs factor
+    (_VectorStore, src/solver.py:84-108): a max pass, then a store pass that
+    also returns sum(load(r)^2) for the residual history;
+  * dots are float64 (K9, deterministic fixed-order reductions);
+  * ||s||^2 comes fused out of the back-projection epilogue.
+
+Persistent vectors live in HBM in the chunked layout [chunks][n][f_dev]
+that the staged SpMM consumes, so an iteration moves no data to the host
+except a handful of scalars.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib, engine, matrixstore
+from .matrixstore import PRECISIONS
+
+__all__ = ["SolveConfig", "SolveResult", "SolverDivergence", "cgls_solve", "early_stop",
+           "residual_curve_report"]
+
+
+class SolverDivergence(RuntimeError):
+    """Raised when an iterate stops being finite (src/solver.py:31-38)."""
+
+    def __init__(self, iteration: int, mode: str, what: str):
+        self.iteration = iteration
+        self.mode = mode
+        super().__init__(f"CGLS diverged at iteration {iteration} in {mode} mode: {what}")
+
+
+@dataclass(frozen=True)
+class SolveConfig:
+    """src/solver.py:41-57."""
+
+    max_iters: int = 30
+    early_stop_iters: int | None = None
+    precision: str = "double"
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if self.early_stop_iters is not None and not (
+                1 <= self.early_stop_iters <= self.max_iters):
+            raise ValueError("early_stop_iters must be in [1, max_iters]")
+        if self.precision not in PRECISIONS:
+            raise ValueError(f"unknown precision {self.precision!r}")
+
+
+@dataclass
+class SolveResult:
+    """src/solver.py:60-81."""
+
+    x: np.ndarray = field(repr=False)
+    residual_history: list = field(default_factory=list)
+    gradient_history: list = field(default_factory=list)
+    iteration_seconds: list = field(default_factory=list)
+    projections: int = 0
+    backprojections: int = 0
+    normalization_factors: list = field(default_factory=list)
+    mode: str = "double"
+
+    @property
+    def iterations(self) -> int:
+        return len(self.residual_history)
+
+
+def early_stop(config: SolveConfig, history: list) -> bool:
+    """src/solver.py:120-126."""
+    if not history:
+        raise ValueError("empty residual history")
+    if config.early_stop_iters is None:
+        return False
+    return len(history) >= config.early_stop_iters
+
+
+def residual_curve_report(histories: dict) -> str:
+    """CSV of relative residuals per mode (src/solver.py:199-223)."""
+    if not histories:
+        raise ValueError("no residual histories to report")
+    modes = sorted(histories)
+    for mode, res in histories.items():
+        if res.iterations == 0:
+            raise ValueError(f"history for mode {mode!r} is empty")
+    depth = max(res.iterations for res in histories.values())
+    header = ["iteration"]
+    for mode in modes:
+        header += [f"{mode}_seconds", f"{mode}_rel_residual"]
+    lines = [",".join(header)]
+    for i in range(depth):
+        row = [str(i + 1)]
+        for mode in modes:
+            res = histories[mode]
+            if i < res.iterations:
+                row += [f"{sum(res.iteration_seconds[:i + 1]):.6e}",
+                        f"{res.residual_history[i]:.9e}"]
+            else:
+                row += ["", ""]
+        lines.append(",".join(row))
+    return "\n".join(lines) + "\n"
+
+
+class _Vec:
+    """A persistent CG vector: payload tensor + dtype code + load factor."""
+
+    __slots__ = ("t", "code", "factor")
+
+    def __init__(self, t, code, factor=1.0):
+        self.t, self.code, self.factor = t, code, factor
+
+
+class DeviceCG:
+    """The device state and kernels of one CGLS solve over one operator."""
+
+    def __init__(self, system, n_slices: int, precision: str):
+        import torch
+        self.sys = system
+        self.dev = system.device
+        self.st = _lib.stream_handle(self.dev)
+        self.prec = precision                       # vector-store policy
+        self.reduced = precision in ("half", "mixed")
+        self.f64 = precision == "double"
+        self.code = 0 if self.f64 else 1            # work dtype code
+        self.wdt = torch.float64 if self.f64 else torch.float32
+        cfg = system.config
+        self.op_prec = cfg.precision
+        self.F = cfg.ffactor
+        self.S = n_slices
+        self.n_chunks = -(-n_slices // self.F)
+        self.f_dev = system.forward.blocks[0].f_dev
+        self.scratch = torch.empty(148 * 8 + 8, dtype=torch.float64, device=self.dev)
+        self.scal = torch.zeros(8, dtype=torch.float64, device=self.dev)
+        self.bits = torch.zeros(max(self.n_chunks, 1), dtype=torch.int64, device=self.dev)
+        sd = {"double": torch.float64, "single": torch.float32}.get(self.op_prec, torch.float16)
+        n_max = max(system.num_rows, system.num_cols)
+        self.xin_buf = torch.empty(self.n_chunks * n_max * self.f_dev, dtype=sd, device=self.dev)
+        self.out_dt = torch.float64 if self.op_prec == "double" else torch.float32
+        blks = [b for s in (system.forward, system.adjoint) for b in s.blocks]
+        self.part_buf = torch.empty(self.n_chunks * max(b.info.n_cta for b in blks),
+                                    dtype=torch.float64, device=self.dev)
+
+    # -- helpers ------------------------------------------------------------------
+    def numel(self, n):
+        return self.n_chunks * n * self.f_dev
+
+    def empty(self, n, dtype=None):
+        import torch
+        return torch.empty(self.numel(n), dtype=dtype or self.wdt, device=self.dev)
+
+    def sum_sq_to_host(self, t, code, factor=1.0):
+        _lib.call("xct_dot", t.data_ptr(), t.data_ptr(), code, t.numel(), float(factor),
+                  float(factor), self.scratch.data_ptr(), self.scal.data_ptr(), self.st)
+        return float(self.scal[0].item())
+
+    def store(self, v_work, out=None) -> _Vec:
+        """_VectorStore.store of a work-dtype vector (src/solver.py:97-103)."""
+        import torch
+        if not self.reduced:
+            return _Vec(v_work, self.code)
+        self.bits.zero_()
+        _lib.call("xct_maxabs", v_work.data_ptr(), 1, v_work.numel(), 1.0, self.bits.data_ptr(),
+                  self.st)
+        peak = float(self.bits[:1].cpu().numpy().view(np.float64)[0])
+        factor = peak if peak > 0 else 1.0
+        if out is None:
+            out = torch.empty(v_work.numel(), dtype=torch.float16, device=self.dev)
+        _lib.call("xct_axpy", v_work.data_ptr(), 1, 1.0, None, 1, 1.0, 0.0, v_work.numel(),
+                  out.data_ptr(), 2, float(np.float32(factor)), None, self.scratch.data_ptr(),
+                  None, self.st)
+        return _Vec(out, 2, factor)
+
+    def update(self, a: _Vec, b: _Vec, scale: float, out_store=None, want_sumsq=False):
+        """out = load(a) + wd(scale) * load(b); stored per the policy.
+        Returns (stored _Vec, sum(load(stored)^2) or None, peak)."""
+        import torch
+        n = a.t.numel()
+        fa, fb = float(np.float32(a.factor)), float(np.float32(b.factor))
+        if not self.reduced:
+            out = out_store if out_store is not None else torch.empty_like(a.t)
+            _lib.call("xct_axpy", a.t.data_ptr(), a.code, fa, b.t.data_ptr(), b.code, fb,
+                      float(scale), n, out.data_ptr(), self.code, 1.0, None, None, None, self.st)
+            ss = self.sum_sq_to_host(out, self.code) if want_sumsq else None
+            return _Vec(out, self.code), ss, None
+        self.bits.zero_()
+        _lib.call("xct_axpy", a.t.data_ptr(), a.code, fa, b.t.data_ptr(), b.code, fb,
+                  float(scale), n, None, 2, 1.0, self.bits.data_ptr(), None, None, self.st)
+        peak = float(self.bits[:1].cpu().numpy().view(np.float64)[0])
+        if not math.isfinite(peak):
+            return None, None, peak
+        factor = peak if peak > 0 else 1.0
+        out = out_store if out_store is not None else torch.empty(n, dtype=torch.float16,
+                                                                  device=self.dev)
+        _lib.call("xct_axpy", a.t.data_ptr(), a.code, fa, b.t.data_ptr(), b.code, fb,
+                  float(scale), n, out.data_ptr(), 2, float(np.float32(factor)), None,
+                  self.scratch.data_ptr(), self.scal.data_ptr() if want_sumsq else None,
+                  self.st)
+        ss = float(self.scal[0].item()) if want_sumsq else None
+        return _Vec(out, 2, factor), ss, peak
+
+    def apply(self, side, v: _Vec, out):
+        """out = op(load(v)) in the chunked layout; returns (factors, ||out||^2)."""
+        import torch
+        n_in, n_out = side.num_inputs, side.num_outputs
+        self.bits.zero_()
+        _lib.call("xct_chunk_maxabs_chunked", v.t.data_ptr(), v.code,
+                  float(np.float32(v.factor)), n_in, self.n_chunks, self.f_dev,
+                  self.bits.data_ptr(), self.st)
+        peaks = self.bits[:self.n_chunks].cpu().numpy().view(np.float64)
+        if not np.all(np.isfinite(peaks)):
+            return None, None
+        factors = [float(p) if p > 0 else 1.0 for p in peaks]
+        fac = torch.tensor(factors, dtype=torch.float64, device=self.dev)
+        xin = self.xin_buf[:self.numel(n_in)].view(self.n_chunks, n_in, self.f_dev)
+        _lib.call("xct_normalize_chunked", v.t.data_ptr(), v.code, float(np.float32(v.factor)),
+                  n_in, self.n_chunks, self.f_dev, fac.data_ptr(), _lib.PREC_CODE[self.op_prec],
+                  xin.data_ptr(), self.st)
+        if len(side.blocks) == 1 and side.input_elements[0] is None:
+            blk = side.blocks[0]
+            parts = self.part_buf[:self.n_chunks * blk.info.n_cta]
+            engine.apply_side(blk, xin, out, row_stride=self.f_dev,
+                              chunk_stride=n_out * self.f_dev,
+                              valid_cols=self.n_chunks * self.f_dev, ffactor_out=self.f_dev,
+                              factors=fac, dot_partials=parts, stream=self.st)
+            _lib.call("xct_sum_f64", parts.data_ptr(), parts.numel(), self.scal.data_ptr(),
+                      self.st)
+            return factors, float(self.scal[0].item())
+        # data-partitioned operator (one-process emulation): strided path on
+        # load(v) in the work dtype, then back to the chunked layout
+        loaded = torch.empty((n_in, self.S), dtype=torch.float64, device=self.dev)
+        _lib.call("xct_unchunk_f64", v.t.data_ptr(), v.code, float(np.float32(v.factor)), n_in,
+                  self.S, self.F, self.f_dev, loaded.data_ptr(), self.st)
+        res, _ = self.sys._apply(side, loaded.to(self.wdt))
+        tmp = res.to(torch.float64).contiguous()
+        oc = 0 if self.out_dt == torch.float64 else 1
+        _lib.call("xct_chunk_from_f64", tmp.data_ptr(), n_out, self.S, self.F, self.f_dev, oc,
+                  out.data_ptr(), self.st)
+        return factors, self.sum_sq_to_host(out, oc)
+
+
+def cgls_solve(system, y, config: SolveConfig) -> SolveResult:
+    """Solve min ||y - A x|| by CGLS on the device (src/solver.py:129-196).
+
+    ``y``: (num_rays,) or (num_rays, slices), numpy or a CUDA tensor.
+    Returns a SolveResult whose ``x`` is float64 numpy (like the reference).
+    """
+    import torch
+    is_np = not isinstance(y, torch.Tensor)
+    yy = np.asarray(y) if is_np else y
+    squeeze = yy.ndim == 1
+    n_rows, n_cols = system.num_rows, system.num_cols
+    if yy.shape[0] != n_rows:
+        raise ValueError(f"measurements have {yy.shape[0]} rays, operator expects {n_rows}")
+    cg = DeviceCG(system, 1 if squeeze else int(yy.shape[1]), config.precision)
+    S, prec = cg.S, config.precision
+    Y = torch.as_tensor(yy, device=cg.dev).to(torch.float64).reshape(n_rows, S).contiguous()
+    result = SolveResult(x=np.zeros(0), mode=prec)
+    cg.bits.zero_()
+    _lib.call("xct_maxabs", Y.data_ptr(), 0, Y.numel(), 1.0, cg.bits.data_ptr(), cg.st)
+    if not math.isfinite(float(cg.bits[:1].cpu().numpy().view(np.float64)[0])):
+        raise SolverDivergence(0, prec, "measurement data contains NaN or Inf")
+    _lib.call("xct_dot", Y.data_ptr(), Y.data_ptr(), 0, Y.numel(), 1.0, 1.0,
+              cg.scratch.data_ptr(), cg.scal.data_ptr(), cg.st)
+    y_sq = float(cg.scal[0].item())
+    y_norm = math.sqrt(y_sq)
+    if y_norm == 0.0:
+        result.x = np.zeros((n_cols,) if squeeze else (n_cols, S))
+        return result
+
+    wdt = cg.wdt
+    x = _Vec(torch.zeros(cg.numel(n_cols), dtype=wdt, device=cg.dev), cg.code)
+    if cg.reduced:
+        x = _Vec(torch.zeros(cg.numel(n_cols), dtype=torch.float16, device=cg.dev), 2, 1.0)
+    r_work = cg.empty(n_rows)
+    _lib.call("xct_chunk_from_f64", Y.data_ptr(), n_rows, S, cg.F, cg.f_dev, cg.code,
+              r_work.data_ptr(), cg.st)
+    del Y
+    r = cg.store(r_work)
+    out_dt = cg.out_dt
+    s_buf = torch.empty(cg.numel(n_cols), dtype=out_dt, device=cg.dev)
+    q_buf = torch.empty(cg.numel(n_rows), dtype=out_dt, device=cg.dev)
+    facs, gamma = cg.apply(system.adjoint, r, s_buf)
+    if facs is None:
+        raise SolverDivergence(0, prec, "residual contains NaN or Inf")
+    result.backprojections += 1
+    result.normalization_factors.append(facs)
+    s_code = 0 if out_dt == torch.float64 else 1
+    s = _Vec(s_buf, s_code)
+    if out_dt != wdt:           # operator dtype differs from the store policy
+        s = _Vec(s_buf.to(wdt), cg.code)
+    p = cg.store(s.t) if cg.reduced else _Vec(s.t.clone(), cg.code)
+    gamma0 = gamma
+
+    for it in range(1, config.max_iters + 1):
+        t0 = time.perf_counter()
+        if gamma == 0.0:
+            break
+        facs, qq = cg.apply(system.forward, p, q_buf)
+        if facs is None:
+            raise SolverDivergence(it, prec, "search direction contains NaN or Inf")
+        result.projections += 1
+        result.normalization_factors.append(facs)
+        if qq == 0.0:
+            break
+        alpha = gamma / qq
+        q = _Vec(q_buf if out_dt == wdt else q_buf.to(wdt), cg.code)
+        x, _, peak = cg.update(x, p, alpha, out_store=x.t)
+        if x is None:
+            raise SolverDivergence(it, prec, "residual contains NaN or Inf")
+        r, rr, peak = cg.update(r, q, -alpha, out_store=r.t, want_sumsq=True)
+        if r is None or not math.isfinite(rr):
+            raise SolverDivergence(it, prec, "residual contains NaN or Inf")
+        facs, gamma_new = cg.apply(system.adjoint, r, s_buf)
+        if facs is None:
+            raise SolverDivergence(it, prec, "residual contains NaN or Inf")
+        result.backprojections += 1
+        result.normalization_factors.append(facs)
+        if not math.isfinite(gamma_new):
+            raise SolverDivergence(it, prec, "gradient norm contains NaN or Inf")
+        beta = gamma_new / gamma if gamma > 0 else 0.0
+        gamma = gamma_new
+        s = _Vec(s_buf if out_dt == wdt else s_buf.to(wdt), cg.code)
+        p, _, _ = cg.update(s, p, beta, out_store=p.t)
+        if p is None:
+            raise SolverDivergence(it, prec, "search direction contains NaN or Inf")
+        result.residual_history.append(math.sqrt(rr) / y_norm)
+        result.gradient_history.append(math.sqrt(gamma_new / gamma0))
+        result.iteration_seconds.append(time.perf_counter() - t0)
+        if early_stop(config, result.residual_history):
+            break
+
+    xf = torch.empty((n_cols, S), dtype=torch.float64, device=cg.dev)
+    _lib.call("xct_unchunk_f64", x.t.data_ptr(), x.code, float(np.float32(x.factor)), n_cols, S,
+              cg.F, cg.f_dev, xf.data_ptr(), cg.st)
+    out = xf.cpu().numpy() if is_np else xf
+    result.x = out[:, 0] if squeeze else out
+    return result

@@ -1,0 +1,161 @@
+"""CPU-only checks of the C ABI library: it loads, exports every symbol the
+header declares, and its host-side format builder (K5) and transpose are
+exact (replayed here against the oracle's matrices)."""
+
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import xct_oracle as O
+from paper_2009_07226_b200 import _lib, matrixstore
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def header_functions():
+    text = (ROOT / "include" / "xct_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(xct_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.lib()
+    names = header_functions()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_lib.exported_symbols())
+    assert lib.xct_abi_version() == 1
+
+
+def test_error_path_reports_message():
+    lib = _lib.lib()
+    st = lib.xct_siddon_count(None, None, 0, 1, 4, 4, 1.0, None, None)
+    assert st == _lib.XCT_EINVAL
+    assert b"angle" in lib.xct_last_error()
+
+
+def export(ip, ix, v, n_rows, n_cols, plan, prec, ff, exp=0, budget=96 * 1024):
+    f_dev = matrixstore.f_dev_for(ff, prec)
+    rec = f_dev * matrixstore.element_bytes(prec)
+    cap = min(65536, budget // rec)
+    h = C.c_void_p()
+    L = _lib.lib()
+    rows = np.ascontiguousarray(plan.cta_rows, np.int32)
+    st = L.xct_format_build(n_rows, n_cols, ip.ctypes.data, ix.ctypes.data, v.ctypes.data,
+                            rows.shape[0], rows.shape[1], plan.rows_per_warp, rows.ctypes.data,
+                            np.ascontiguousarray(plan.key_tables, np.int32).ctypes.data,
+                            np.ascontiguousarray(plan.cta_table, np.int32).ctypes.data, cap,
+                            _lib.PREC_CODE[prec], exp, 4, C.byref(h))
+    _lib.check(st, "build")
+    info = _lib.FormatInfo()
+    L.xct_format_get_info(h, C.byref(info))
+    w = info.warps_per_cta
+    a = dict(gp=np.empty(info.n_cta + 1, np.int32), mp=np.empty(info.n_groups + 1, np.int64),
+             m=np.empty(max(1, info.n_slots), np.int32),
+             so=np.empty(max(1, info.n_groups * w), np.int64),
+             sw=np.empty(max(1, info.n_groups * w), np.int32),
+             sl=np.empty(max(1, info.n_padded), np.uint16),
+             v=np.empty(max(1, info.n_padded), matrixstore.storage_dtype(prec)))
+    L.xct_format_export(h, *[a[k].ctypes.data for k in ("gp", "mp", "m", "so", "sw", "sl", "v")])
+    L.xct_format_free(h)
+    return info, a, rows, cap
+
+
+def replay(info, a, rows, n_rows):
+    """Per-row (column, value) sequences in accumulation order."""
+    seqs = {r: [] for r in range(n_rows)}
+    rpw, w = info.rows_per_warp, info.warps_per_cta
+    for b in range(info.n_cta):
+        for g in range(a["gp"][b], a["gp"][b + 1]):
+            gmap = a["m"][a["mp"][g]:a["mp"][g + 1]]
+            for wi in range(w):
+                off, width = a["so"][g * w + wi], a["sw"][g * w + wi]
+                assert width % 4 == 0
+                for rin in range(rpw):
+                    r = rows[b, wi * rpw + rin]
+                    for n in range(width):
+                        at = off + ((n // 4) * rpw + rin) * 4 + n % 4
+                        val = a["v"][at]
+                        if r < 0:
+                            assert val == 0
+                            continue
+                        if val != 0:
+                            seqs[r].append((int(gmap[a["sl"][at]]), float(val)))
+    return seqs
+
+
+@pytest.mark.parametrize("prec", ["double", "single", "mixed"])
+def test_format_builder_native_and_reference_orders(prec):
+    g = O.make_geom(24, 1, 16)
+    A = O.system_matrix(g)
+    ip, ix, v = A.indptr, A.indices.astype(np.int32), A.values
+    rw = 32 // matrixstore.lanes_for(4, prec)
+    exp = O.rescale_exp(v) if prec == "mixed" else 0
+    # native: forward band staging keeps traversal order in every row
+    plan = matrixstore.assign_forward_regimes(
+        matrixstore.forward_plan(g.num_angles, g.n, rw, 4), g.angles, g.n)
+    info, a, rows, _ = export(ip, ix, v, A.num_rows, A.num_cols, plan, prec, 4, exp,
+                              budget=2048)
+    assert info.n_groups > info.n_cta          # several load groups per tile
+    seqs = replay(info, a, rows, A.num_rows)
+    sd = matrixstore.storage_dtype(prec)
+    for r in range(A.num_rows):
+        s, e = ip[r], ip[r + 1]
+        want = [(int(c), float(sd(val * 2.0 ** exp))) for c, val in zip(ix[s:e], v[s:e])]
+        assert seqs[r] == want, r
+    # reference: per-row order = (reference stage, traversal)
+    plan = matrixstore.reference_plan(ip, ix, A.num_rows, A.num_cols, 4, 1024, 4, prec, rw, 4)
+    info, a, rows, _ = export(ip, ix, v, A.num_rows, A.num_cols, plan, prec, 4, exp)
+    seqs = replay(info, a, rows, A.num_rows)
+    row, perm = O.stage_order(O.whole_block(A), 1024, 4, 4, prec)
+    for r in range(A.num_rows):
+        s, e = ip[r], ip[r + 1]
+        order = [p for p in perm[s:e]]
+        want = [(int(ix[p]), float(sd(v[p] * 2.0 ** exp))) for p in order]
+        assert seqs[r] == want, r
+
+
+def test_format_builder_adjoint_ray_order_and_capacity_error():
+    g = O.make_geom(20, 1, 16)
+    A = O.system_matrix(g)
+    T = O.transpose_block(O.whole_block(A))
+    ip, ix, v = T.indptr, T.indices.astype(np.int32), T.values
+    plan = matrixstore.adjoint_plan(g.num_angles, g.n, 8, 4)
+    info, a, rows, _ = export(ip, ix, v, T.num_rows, T.num_cols, plan, "single", 16,
+                              budget=64 * 64)
+    seqs = replay(info, a, rows, T.num_rows)
+    for r in range(T.num_rows):
+        s, e = ip[r], ip[r + 1]
+        assert [c for c, _ in seqs[r]] == ix[s:e].tolist()       # ascending ray id
+    with pytest.raises(matrixstore.StageSplitRequired):
+        export(ip, ix, v, T.num_rows, T.num_cols, plan, "single", 16, budget=64 * 4)
+
+
+def test_csr_transpose_is_the_reference_transpose():
+    g = O.make_geom(12, 1, 16)
+    A = O.system_matrix(g)
+    T = O.transpose_block(O.whole_block(A))
+    from paper_2009_07226_b200.pipeline import _transpose
+    t_ip, t_ix, t_v = _transpose(A.indptr, A.indices.astype(np.int32), A.values,
+                                 A.num_rows, A.num_cols)
+    assert np.array_equal(t_ip, T.indptr)
+    assert np.array_equal(t_ix, T.indices)
+    assert np.array_equal(t_v, T.values)
+
+
+def test_f64_to_f16_matches_numpy():
+    # the builder's direct f64 -> f16 RNE cast (pack, src/matrixstore.py:260)
+    rng = np.random.default_rng(0)
+    vals = np.concatenate([rng.random(2000) * 2.0, rng.random(200) * 1e-6,
+                           [65519.99, 65520.0, 6.1e-5, 5.96e-8, 2.98e-8, 1.0 + 2**-11]])
+    ip = np.arange(len(vals) + 1, dtype=np.int64)
+    ix = np.zeros(len(vals), np.int32)
+    plan = matrixstore.row_block_plan(len(vals), 1, 16, 1)
+    info, a, rows, _ = export(ip, ix, vals, len(vals), 1, plan, "mixed", 16)
+    seqs = replay(info, a, rows, len(vals))
+    got = np.array([seqs[r][0][1] if seqs[r] else 0.0 for r in range(len(vals))])
+    assert np.array_equal(got, vals.astype(np.float16).astype(np.float64))
