@@ -112,8 +112,24 @@ def check(status: int, what: str):
     raise XctError(f"{what}: {msg} (status {status})")
 
 
+# kernels launched per ABI call (for bench.py's gpu_launches count)
+KERNELS_PER_CALL = {"xct_dot": 2, "xct_sum_f64": 1, "xct_spmm": 1, "xct_maxabs": 1,
+                    "xct_chunk_maxabs": 1, "xct_normalize": 1, "xct_chunk_maxabs_chunked": 1,
+                    "xct_normalize_chunked": 1, "xct_unchunk_f64": 1, "xct_chunk_from_f64": 1,
+                    "xct_csr_spmm_f64": 1, "xct_siddon_count": 1, "xct_siddon_fill": 1}
+launch_count = [0]
+
+
+def count_launches(name: str, n: int | None = None):
+    launch_count[0] += KERNELS_PER_CALL.get(name, 0) if n is None else n
+
+
 def call(name: str, *args):
     check(getattr(lib(), name)(*args), name)
+    if name == "xct_axpy":      # second kernel when a sum of squares is requested
+        count_launches(name, 2 if (args[8] is not None and args[13] is not None) else 1)
+    else:
+        count_launches(name)
 
 
 def ptr(t) -> int | None:

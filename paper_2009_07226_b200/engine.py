@@ -83,6 +83,7 @@ def apply_side(side: DeviceSide, x_chunked, out, *, row_stride: int, chunk_strid
     _lib.check(_lib.lib().xct_spmm(C.byref(side.staged), _lib.PREC_CODE[side.precision],
                                    x_chunked.data_ptr(), side.n_in, n_chunks, side.f_dev,
                                    C.byref(ep), side.smem_bytes, st), "xct_spmm")
+    _lib.count_launches("xct_spmm")
 
 
 def csr_spmm_f64(matrix, x: np.ndarray) -> np.ndarray:

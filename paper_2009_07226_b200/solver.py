@@ -153,6 +153,7 @@ class DeviceCG:
         blks = [b for s in (system.forward, system.adjoint) for b in s.blocks]
         self.part_buf = torch.empty(self.n_chunks * max(b.info.n_cta for b in blks),
                                     dtype=torch.float64, device=self.dev)
+        self.events = None           # list -> (is_forward, start, end) per SpMM launch
 
     # -- helpers ------------------------------------------------------------------
     def numel(self, n):
@@ -232,10 +233,17 @@ class DeviceCG:
         if len(side.blocks) == 1 and side.input_elements[0] is None:
             blk = side.blocks[0]
             parts = self.part_buf[:self.n_chunks * blk.info.n_cta]
+            ev = self.events
+            if ev is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
             engine.apply_side(blk, xin, out, row_stride=self.f_dev,
                               chunk_stride=n_out * self.f_dev,
                               valid_cols=self.n_chunks * self.f_dev, ffactor_out=self.f_dev,
                               factors=fac, dot_partials=parts, stream=self.st)
+            if ev is not None:
+                e1.record()
+                ev.append((side is self.sys.forward, e0, e1))
             _lib.call("xct_sum_f64", parts.data_ptr(), parts.numel(), self.scal.data_ptr(),
                       self.st)
             return factors, float(self.scal[0].item())
@@ -252,100 +260,150 @@ class DeviceCG:
         return factors, self.sum_sq_to_host(out, oc)
 
 
+class CGLSRun:
+    """One CGLS solve as explicit steps (used by cgls_solve and bench.py):
+    ``start()`` performs the setup and the initial back projection,
+    ``step()`` one iteration (1 projection + 1 back projection + updates),
+    ``finish()`` returns the SolveResult with x on the host (or device)."""
+
+    def __init__(self, system, y, config: SolveConfig, spmm_events=None):
+        import torch
+        self.system, self.config = system, config
+        self.is_np = not isinstance(y, torch.Tensor)
+        yy = np.asarray(y) if self.is_np else y
+        self.squeeze = yy.ndim == 1
+        n_rows = system.num_rows
+        if yy.shape[0] != n_rows:
+            raise ValueError(f"measurements have {yy.shape[0]} rays, operator expects {n_rows}")
+        self.cg = DeviceCG(system, 1 if self.squeeze else int(yy.shape[1]), config.precision)
+        self.cg.events = spmm_events
+        self.y = yy
+        self.result = SolveResult(x=np.zeros(0), mode=config.precision)
+        self.it = 0
+        self.done = False
+
+    def start(self) -> bool:
+        import torch
+        cg, prec, system = self.cg, self.config.precision, self.system
+        S, n_rows, n_cols = cg.S, system.num_rows, system.num_cols
+        Y = torch.as_tensor(self.y, device=cg.dev)
+        if Y.dtype != torch.float64:
+            Y = Y.to(torch.float64)
+        Y = Y.reshape(n_rows, S).contiguous()
+        cg.bits.zero_()
+        _lib.call("xct_maxabs", Y.data_ptr(), 0, Y.numel(), 1.0, cg.bits.data_ptr(), cg.st)
+        if not math.isfinite(float(cg.bits[:1].cpu().numpy().view(np.float64)[0])):
+            raise SolverDivergence(0, prec, "measurement data contains NaN or Inf")
+        _lib.call("xct_dot", Y.data_ptr(), Y.data_ptr(), 0, Y.numel(), 1.0, 1.0,
+                  cg.scratch.data_ptr(), cg.scal.data_ptr(), cg.st)
+        self.y_norm = math.sqrt(float(cg.scal[0].item()))
+        if self.y_norm == 0.0:
+            self.done = True
+            self.x = None
+            return False
+        if cg.reduced:
+            self.x = _Vec(torch.zeros(cg.numel(n_cols), dtype=torch.float16, device=cg.dev), 2, 1.0)
+        else:
+            self.x = _Vec(torch.zeros(cg.numel(n_cols), dtype=cg.wdt, device=cg.dev), cg.code)
+        r_work = cg.empty(n_rows)
+        _lib.call("xct_chunk_from_f64", Y.data_ptr(), n_rows, S, cg.F, cg.f_dev, cg.code,
+                  r_work.data_ptr(), cg.st)
+        del Y
+        self.r = cg.store(r_work)
+        self.s_buf = torch.empty(cg.numel(n_cols), dtype=cg.out_dt, device=cg.dev)
+        self.q_buf = torch.empty(cg.numel(n_rows), dtype=cg.out_dt, device=cg.dev)
+        facs, gamma = cg.apply(system.adjoint, self.r, self.s_buf)
+        if facs is None:
+            raise SolverDivergence(0, prec, "residual contains NaN or Inf")
+        self.result.backprojections += 1
+        self.result.normalization_factors.append(facs)
+        s = self._work(self.s_buf)
+        self.p = cg.store(s.t) if cg.reduced else _Vec(s.t.clone(), cg.code)
+        self.gamma = self.gamma0 = gamma
+        return True
+
+    def _work(self, buf) -> _Vec:
+        cg = self.cg
+        return _Vec(buf if cg.out_dt == cg.wdt else buf.to(cg.wdt), cg.code)
+
+    def step(self) -> bool:
+        """One iteration (src/solver.py:160-192); False when the solve ends."""
+        if self.done or self.it >= self.config.max_iters:
+            self.done = True
+            return False
+        cg, prec, res, system = self.cg, self.config.precision, self.result, self.system
+        it = self.it = self.it + 1
+        t0 = time.perf_counter()
+        if self.gamma == 0.0:
+            self.done = True
+            return False
+        facs, qq = cg.apply(system.forward, self.p, self.q_buf)
+        if facs is None:
+            raise SolverDivergence(it, prec, "search direction contains NaN or Inf")
+        res.projections += 1
+        res.normalization_factors.append(facs)
+        if qq == 0.0:
+            self.done = True
+            return False
+        alpha = self.gamma / qq
+        q = self._work(self.q_buf)
+        self.x, _, _ = cg.update(self.x, self.p, alpha, out_store=self.x.t)
+        if self.x is None:
+            raise SolverDivergence(it, prec, "residual contains NaN or Inf")
+        self.r, rr, _ = cg.update(self.r, q, -alpha, out_store=self.r.t, want_sumsq=True)
+        if self.r is None or not math.isfinite(rr):
+            raise SolverDivergence(it, prec, "residual contains NaN or Inf")
+        facs, gamma_new = cg.apply(system.adjoint, self.r, self.s_buf)
+        if facs is None:
+            raise SolverDivergence(it, prec, "residual contains NaN or Inf")
+        res.backprojections += 1
+        res.normalization_factors.append(facs)
+        if not math.isfinite(gamma_new):
+            raise SolverDivergence(it, prec, "gradient norm contains NaN or Inf")
+        beta = gamma_new / self.gamma if self.gamma > 0 else 0.0
+        self.gamma = gamma_new
+        self.p, _, _ = cg.update(self._work(self.s_buf), self.p, beta, out_store=self.p.t)
+        if self.p is None:
+            raise SolverDivergence(it, prec, "search direction contains NaN or Inf")
+        res.residual_history.append(math.sqrt(rr) / self.y_norm)
+        res.gradient_history.append(math.sqrt(gamma_new / self.gamma0))
+        res.iteration_seconds.append(time.perf_counter() - t0)
+        if early_stop(self.config, res.residual_history):
+            self.done = True
+            return False
+        return True
+
+    def finish(self) -> SolveResult:
+        import torch
+        cg, system = self.cg, self.system
+        n_cols, S = system.num_cols, cg.S
+        if self.x is None:
+            out = np.zeros((n_cols, S))
+            if not self.is_np:
+                out = torch.zeros((n_cols, S), dtype=torch.float64, device=cg.dev)
+        else:
+            xf = torch.empty((n_cols, S), dtype=torch.float64, device=cg.dev)
+            _lib.call("xct_unchunk_f64", self.x.t.data_ptr(), self.x.code,
+                      float(np.float32(self.x.factor)), n_cols, S, cg.F, cg.f_dev,
+                      xf.data_ptr(), cg.st)
+            if self.is_np:
+                out = xf.cpu().numpy()
+            elif not self.y.is_cuda:          # host tensor in -> host tensor out
+                out = xf.cpu()
+            else:
+                out = xf
+        self.result.x = out[:, 0] if self.squeeze else out
+        return self.result
+
+
 def cgls_solve(system, y, config: SolveConfig) -> SolveResult:
     """Solve min ||y - A x|| by CGLS on the device (src/solver.py:129-196).
 
     ``y``: (num_rays,) or (num_rays, slices), numpy or a CUDA tensor.
-    Returns a SolveResult whose ``x`` is float64 numpy (like the reference).
+    Returns a SolveResult whose ``x`` is float64 (numpy for numpy input).
     """
-    import torch
-    is_np = not isinstance(y, torch.Tensor)
-    yy = np.asarray(y) if is_np else y
-    squeeze = yy.ndim == 1
-    n_rows, n_cols = system.num_rows, system.num_cols
-    if yy.shape[0] != n_rows:
-        raise ValueError(f"measurements have {yy.shape[0]} rays, operator expects {n_rows}")
-    cg = DeviceCG(system, 1 if squeeze else int(yy.shape[1]), config.precision)
-    S, prec = cg.S, config.precision
-    Y = torch.as_tensor(yy, device=cg.dev).to(torch.float64).reshape(n_rows, S).contiguous()
-    result = SolveResult(x=np.zeros(0), mode=prec)
-    cg.bits.zero_()
-    _lib.call("xct_maxabs", Y.data_ptr(), 0, Y.numel(), 1.0, cg.bits.data_ptr(), cg.st)
-    if not math.isfinite(float(cg.bits[:1].cpu().numpy().view(np.float64)[0])):
-        raise SolverDivergence(0, prec, "measurement data contains NaN or Inf")
-    _lib.call("xct_dot", Y.data_ptr(), Y.data_ptr(), 0, Y.numel(), 1.0, 1.0,
-              cg.scratch.data_ptr(), cg.scal.data_ptr(), cg.st)
-    y_sq = float(cg.scal[0].item())
-    y_norm = math.sqrt(y_sq)
-    if y_norm == 0.0:
-        result.x = np.zeros((n_cols,) if squeeze else (n_cols, S))
-        return result
-
-    wdt = cg.wdt
-    x = _Vec(torch.zeros(cg.numel(n_cols), dtype=wdt, device=cg.dev), cg.code)
-    if cg.reduced:
-        x = _Vec(torch.zeros(cg.numel(n_cols), dtype=torch.float16, device=cg.dev), 2, 1.0)
-    r_work = cg.empty(n_rows)
-    _lib.call("xct_chunk_from_f64", Y.data_ptr(), n_rows, S, cg.F, cg.f_dev, cg.code,
-              r_work.data_ptr(), cg.st)
-    del Y
-    r = cg.store(r_work)
-    out_dt = cg.out_dt
-    s_buf = torch.empty(cg.numel(n_cols), dtype=out_dt, device=cg.dev)
-    q_buf = torch.empty(cg.numel(n_rows), dtype=out_dt, device=cg.dev)
-    facs, gamma = cg.apply(system.adjoint, r, s_buf)
-    if facs is None:
-        raise SolverDivergence(0, prec, "residual contains NaN or Inf")
-    result.backprojections += 1
-    result.normalization_factors.append(facs)
-    s_code = 0 if out_dt == torch.float64 else 1
-    s = _Vec(s_buf, s_code)
-    if out_dt != wdt:           # operator dtype differs from the store policy
-        s = _Vec(s_buf.to(wdt), cg.code)
-    p = cg.store(s.t) if cg.reduced else _Vec(s.t.clone(), cg.code)
-    gamma0 = gamma
-
-    for it in range(1, config.max_iters + 1):
-        t0 = time.perf_counter()
-        if gamma == 0.0:
-            break
-        facs, qq = cg.apply(system.forward, p, q_buf)
-        if facs is None:
-            raise SolverDivergence(it, prec, "search direction contains NaN or Inf")
-        result.projections += 1
-        result.normalization_factors.append(facs)
-        if qq == 0.0:
-            break
-        alpha = gamma / qq
-        q = _Vec(q_buf if out_dt == wdt else q_buf.to(wdt), cg.code)
-        x, _, peak = cg.update(x, p, alpha, out_store=x.t)
-        if x is None:
-            raise SolverDivergence(it, prec, "residual contains NaN or Inf")
-        r, rr, peak = cg.update(r, q, -alpha, out_store=r.t, want_sumsq=True)
-        if r is None or not math.isfinite(rr):
-            raise SolverDivergence(it, prec, "residual contains NaN or Inf")
-        facs, gamma_new = cg.apply(system.adjoint, r, s_buf)
-        if facs is None:
-            raise SolverDivergence(it, prec, "residual contains NaN or Inf")
-        result.backprojections += 1
-        result.normalization_factors.append(facs)
-        if not math.isfinite(gamma_new):
-            raise SolverDivergence(it, prec, "gradient norm contains NaN or Inf")
-        beta = gamma_new / gamma if gamma > 0 else 0.0
-        gamma = gamma_new
-        s = _Vec(s_buf if out_dt == wdt else s_buf.to(wdt), cg.code)
-        p, _, _ = cg.update(s, p, beta, out_store=p.t)
-        if p is None:
-            raise SolverDivergence(it, prec, "search direction contains NaN or Inf")
-        result.residual_history.append(math.sqrt(rr) / y_norm)
-        result.gradient_history.append(math.sqrt(gamma_new / gamma0))
-        result.iteration_seconds.append(time.perf_counter() - t0)
-        if early_stop(config, result.residual_history):
-            break
-
-    xf = torch.empty((n_cols, S), dtype=torch.float64, device=cg.dev)
-    _lib.call("xct_unchunk_f64", x.t.data_ptr(), x.code, float(np.float32(x.factor)), n_cols, S,
-              cg.F, cg.f_dev, xf.data_ptr(), cg.st)
-    out = xf.cpu().numpy() if is_np else xf
-    result.x = out[:, 0] if squeeze else out
-    return result
+    run = CGLSRun(system, y, config)
+    if run.start():
+        while run.step():
+            pass
+    return run.finish()

@@ -142,6 +142,12 @@ def test_c1_reference_order_bit_exact(golden_manifest):
 
 
 def test_c1_native_order_tolerances():
+    """Native band staging accumulates every ray in traversal order, i.e. the
+    reference's own order for stage_capacity_bytes=None, block_partitions=1:
+    bit-identical to that configuration, and within twice the reference's
+    own order-noise floor of its default configuration (measured with the
+    oracle: residual curve 2.5-7.1 % single / 1.3 % mixed, x 6.5e-4..1.6e-3
+    single / 1.2e-3 mixed at 30 iterations)."""
     gold = load_golden("c1")
     g = geometry.make_geometry(180, 16, 128)
     og = O.make_geom(180, 16, 128)
@@ -151,13 +157,14 @@ def test_c1_native_order_tolerances():
         sysm = pipeline.assemble(g, pipeline.SystemConfig(precision=prec, ffactor=16))
         res10 = solver.cgls_solve(sysm, y, solver.SolveConfig(max_iters=10, precision=prec))
         ref10 = O.cgls(O.Operator(OA, og, prec, 16), y, 10, prec)
-        tol = 1e-5 if prec == "single" else 2e-2
-        assert rel_l2(res10.x, ref10["x"]) <= tol, prec
+        assert rel_l2(res10.x, ref10["x"]) <= 1e-5, prec
+        same = O.cgls(O.Operator(OA, og, prec, 16, partitions=1, cap_bytes=None), y, 10, prec)
+        assert np.array_equal(res10.x, same["x"]), prec
         res = solver.cgls_solve(sysm, y, solver.SolveConfig(max_iters=30, precision=prec))
         curve = gold[f"cg_{prec}_residual"]
-        assert np.max(np.abs(np.array(res.residual_history) / curve - 1)) <= 0.02
-        # measured reference noise floor at 30 its: 6.5e-4..1.6e-3 (single)
-        assert rel_l2(res.x, gold[f"cg_{prec}_x"]) <= (5e-3 if prec == "single" else 2e-2)
+        floor_curve, floor_x = (0.071, 1.6e-3) if prec == "single" else (0.013, 1.2e-3)
+        assert np.max(np.abs(np.array(res.residual_history) / curve - 1)) <= 2 * floor_curve
+        assert rel_l2(res.x, gold[f"cg_{prec}_x"]) <= 2 * floor_x
 
 
 def test_cgls_g90_all_precisions():
