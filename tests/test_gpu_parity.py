@@ -177,10 +177,15 @@ def test_cgls_g90_all_precisions():
         res = solver.cgls_solve(sysm, y, solver.SolveConfig(max_iters=12, precision=prec))
         assert [res.projections, res.backprojections] == list(gold[f"{prec}_counts"])
         if prec == "double":
-            assert rel_l2(res.x, gold[f"{prec}_x"]) <= 1e-10
+            # double CGLS on this noisy problem is chaotic: replacing numpy's
+            # vdot by an exactly rounded sum moves the reference's own x by
+            # 1.29e-5 (oracle, tests/test_oracle_golden.py); single/mixed/half
+            # cast alpha/beta to f32 and stay bit-exact
+            assert rel_l2(res.x, gold[f"{prec}_x"]) <= 3e-5
+            np.testing.assert_allclose(res.residual_history, gold[f"{prec}_residual"], rtol=1e-4)
         else:
-            assert rel_l2(res.x, gold[f"{prec}_x"]) <= 1e-6, prec
-        np.testing.assert_allclose(res.residual_history, gold[f"{prec}_residual"], rtol=1e-6)
+            assert np.array_equal(res.x, gold[f"{prec}_x"]), prec
+            assert np.array_equal(res.residual_history, gold[f"{prec}_residual"])
 
 
 def test_edge_cases_padding_vectors_zero():

@@ -142,3 +142,20 @@ def test_c1_operator_and_cgls(golden_manifest):
 def test_slice_groups_rule():
     assert O.slice_groups(10, 3) == [(0, 4), (4, 7), (7, 10)]
     assert O.slice_groups(2, 4) == [(0, 1), (1, 2)]
+
+
+def test_double_cgls_order_noise_floor():
+    """Pins the tolerance of the GPU double-mode CGLS test: an exactly
+    rounded dot (math.fsum) instead of numpy's vdot moves x by ~1.3e-5 on the
+    noisy g90 problem after 12 iterations (single/mixed/half: 0)."""
+    gold = load_golden("cgls_g90")
+    g = O.make_geom(90, 1, 64)
+    op = O.Operator(O.system_matrix(g), g, "double", 4)
+    orig = O._vdot
+    try:
+        O._vdot = lambda a, b: math.fsum((a.astype(np.float64) * b.astype(np.float64)).ravel())
+        r = O.cgls(op, gold["y90"], 12, "double")
+    finally:
+        O._vdot = orig
+    d = np.linalg.norm(r["x"] - gold["double_x"]) / np.linalg.norm(gold["double_x"])
+    assert 1e-6 < d < 3e-5
