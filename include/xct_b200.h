@@ -70,6 +70,13 @@ int xct_siddon_fill(const double* d_cos, const double* d_sin, int k0, int k1,
  * accumulated group by group, in (key, CSR position) order inside a group.
  * Per (group, warp) the entries of the warp's rows are stored as a
  * zero-padded slab [width/4][rows_per_warp][4] of (uint16 slot, value).
+ * sched_log2_pieces >= 0 enables bank-conflict-free scheduling for a kernel
+ * whose records are 2^sched_log2_pieces 16-byte pieces read by
+ * 2^sched_log2_lanes lanes per row: within each (group, warp, quarter-warp)
+ * the entries are placed on slab steps by a proper edge colouring of the
+ * rows x shared-memory-bank-class multigraph, so no two rows of a quarter
+ * read the same bank quads in one step (row order is then not traversal
+ * order; sums agree to rounding).  -1 keeps (key, CSR position) order.
  * ------------------------------------------------------------------------- */
 typedef struct xct_format xct_format;
 
@@ -89,6 +96,7 @@ int xct_format_build(int64_t n_rows, int64_t n_cols,
                      const int32_t* h_cta_rows,
                      const int32_t* h_key_tables, const int32_t* h_cta_table,
                      int64_t capacity, int precision, int value_scale_exp,
+                     int sched_log2_pieces, int sched_log2_lanes,
                      int n_threads, xct_format** out);
 int xct_format_get_info(const xct_format* f, xct_format_info* info);
 /* copies the format arrays into caller-provided host buffers sized from

@@ -50,7 +50,7 @@ _SIGS = {
     "xct_siddon_count": (i32, [vp, vp, i32, i32, i32, i32, f64, vp, vp]),
     "xct_siddon_fill": (i32, [vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp]),
     "xct_format_build": (i32, [i64, i64, vp, vp, vp, i64, i64, i64, vp, vp, vp, i64, i32,
-                               i32, i32, C.POINTER(vp)]),
+                               i32, i32, i32, i32, C.POINTER(vp)]),
     "xct_format_get_info": (i32, [vp, C.POINTER(FormatInfo)]),
     "xct_format_export": (i32, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "xct_format_free": (None, [vp]),

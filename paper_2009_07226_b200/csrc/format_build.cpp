@@ -68,6 +68,93 @@ struct CtaPlan {
   std::vector<int32_t> width;        // [n_groups_local * warps] padded widths
 };
 
+// Shared-memory bank class of a slot for the lanes of one row (mirrors the
+// plane layout of spmm.cu: piece p of slot s sits at bank quad
+// (s + p*8/NP) mod 8, the L lanes of a row read pieces L apart).  Two rows of
+// a quarter-warp conflict iff their slots agree mod 8/L.
+struct BankModel {
+  int lp = -1, lg = 0, rq = 0;   // log2 pieces, log2 lanes per row, rows per quarter
+  bool on() const { return lp >= 0 && rq > 1; }
+  void init(int log2_pieces, int log2_lanes) {
+    lp = log2_pieces;
+    lg = log2_lanes;
+    rq = lg <= 3 ? (8 >> lg) : 1;
+  }
+  int cls(int64_t slot) const { return (int)(slot & (rq - 1)); }
+};
+
+// Proper edge colouring of a bipartite multigraph rows x bank classes with
+// `ncolor` >= max degree colours (Konig): colour = step of the slab, so no
+// two rows of a quarter-warp read the same bank quads in one step.
+struct Colorer {
+  int ncolor = 0, words = 0;
+  std::vector<int32_t> atL, atR;        // [vertex * ncolor + colour] -> edge or -1
+  std::vector<uint64_t> freeL, freeR;   // free-colour bitmaps
+  std::vector<int32_t> er, ec, col;
+  std::vector<int32_t> path;
+
+  void reset(int nl, int nr, int nc) {
+    ncolor = nc;
+    words = (nc + 63) / 64;
+    atL.assign((size_t)nl * nc, -1);
+    atR.assign((size_t)nr * nc, -1);
+    freeL.assign((size_t)nl * words, ~0ull);
+    freeR.assign((size_t)nr * words, ~0ull);
+    for (int v = 0; v < nl; ++v) trim(freeL, v);
+    for (int v = 0; v < nr; ++v) trim(freeR, v);
+    er.clear(); ec.clear(); col.clear();
+  }
+  void trim(std::vector<uint64_t>& f, int v) {
+    int rem = ncolor % 64;
+    if (rem) f[(size_t)v * words + words - 1] = (1ull << rem) - 1;
+  }
+  int first_free(const std::vector<uint64_t>& f, int v) const {
+    for (int w = 0; w < words; ++w) {
+      uint64_t m = f[(size_t)v * words + w];
+      if (m) return w * 64 + __builtin_ctzll(m);
+    }
+    return -1;
+  }
+  void put(int e, int c) {
+    col[e] = c;
+    atL[(size_t)er[e] * ncolor + c] = e;
+    atR[(size_t)ec[e] * ncolor + c] = e;
+    freeL[(size_t)er[e] * words + c / 64] &= ~(1ull << (c % 64));
+    freeR[(size_t)ec[e] * words + c / 64] &= ~(1ull << (c % 64));
+  }
+  void take(int e) {
+    int c = col[e];
+    atL[(size_t)er[e] * ncolor + c] = -1;
+    atR[(size_t)ec[e] * ncolor + c] = -1;
+    freeL[(size_t)er[e] * words + c / 64] |= 1ull << (c % 64);
+    freeR[(size_t)ec[e] * words + c / 64] |= 1ull << (c % 64);
+  }
+  bool add(int l, int r) {
+    int e = (int)er.size();
+    er.push_back(l); ec.push_back(r); col.push_back(-1);
+    int a = first_free(freeL, l), b = first_free(freeR, r);
+    if (a < 0 || b < 0) return false;
+    if (atR[(size_t)r * ncolor + a] >= 0) {
+      // flip the a/b alternating path that starts at r; it cannot reach l
+      path.clear();
+      int v = r, want = a;
+      bool right = true;
+      for (;;) {
+        int e2 = right ? atR[(size_t)v * ncolor + want] : atL[(size_t)v * ncolor + want];
+        if (e2 < 0) break;
+        path.push_back(e2);
+        v = right ? er[e2] : ec[e2];
+        right = !right;
+        want = want == a ? b : a;
+      }
+      for (int e2 : path) take(e2);
+      for (int e2 : path) put(e2, col[e2] == a ? b : a);
+    }
+    put(e, a);
+    return true;
+  }
+};
+
 }  // namespace
 
 struct xct_format {
@@ -107,7 +194,8 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
                                 int64_t n_cta, int64_t rows_per_cta, int64_t rows_per_warp,
                                 const int32_t* cta_rows, const int32_t* key_tables,
                                 const int32_t* cta_table, int64_t capacity, int precision,
-                                int value_scale_exp, int n_threads, xct_format** out) {
+                                int value_scale_exp, int sched_log2_pieces,
+                                int sched_log2_lanes, int n_threads, xct_format** out) {
   if (!out) return xct::fail(XCT_EINVAL, "format_build: null output handle");
   *out = nullptr;
   if (n_rows < 0 || n_cols < 0 || n_cta < 0 || rows_per_cta < 1 || rows_per_warp < 1 ||
@@ -121,6 +209,13 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
   const int64_t warps = rows_per_cta / rows_per_warp;
   const int vbytes = precision == XCT_DOUBLE ? 8 : precision == XCT_SINGLE ? 4 : 2;
 
+  BankModel bank;
+  if (sched_log2_pieces >= 0) {
+    if (sched_log2_lanes < 0 || sched_log2_lanes > sched_log2_pieces ||
+        (32 >> sched_log2_lanes) != rows_per_warp)
+      return xct::fail(XCT_EINVAL, "format_build: schedule lanes do not match rows_per_warp");
+    bank.init(sched_log2_pieces, sched_log2_lanes);
+  }
   std::vector<CtaPlan> plans(n_cta);
   std::mutex err_mu;
   int err = XCT_OK;
@@ -165,20 +260,39 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
     P.width.assign(ng * warps, 0);
     // the key is a function of the column, so the column alone locates an
     // entry in the footprint: dense per-thread lookup tables
-    static thread_local std::vector<int32_t> group_of;
-    if ((int64_t)group_of.size() < n_cols) group_of.assign(n_cols, 0);
+    static thread_local std::vector<int32_t> group_of, cls_of;
+    if ((int64_t)group_of.size() < n_cols) { group_of.assign(n_cols, 0); cls_of.assign(n_cols, 0); }
     for (int64_t g = 0; g < ng; ++g)
-      for (int64_t p = P.gstart[g]; p < P.gstart[g + 1]; ++p) group_of[P.foot[p].col] = (int32_t)g;
+      for (int64_t p = P.gstart[g]; p < P.gstart[g + 1]; ++p) {
+        group_of[P.foot[p].col] = (int32_t)g;
+        if (bank.on()) cls_of[P.foot[p].col] = bank.cls(p - P.gstart[g]);
+      }
     std::vector<int32_t> cnt(ng);
+    // per (group, quarter) bank-class loads of the current warp
+    std::vector<int32_t> ccnt(bank.on() ? ng * 8 : 0);
+    const int64_t rq = bank.on() ? bank.rq : rows_per_warp;
     for (int64_t t = 0; t < rows_per_cta; ++t) {
-      int32_t r = cta_rows[b * rows_per_cta + t];
-      if (r < 0) continue;
-      std::fill(cnt.begin(), cnt.end(), 0);
-      for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) ++cnt[group_of[indices[j]]];
       int64_t w = t / rows_per_warp;
-      for (int64_t g = 0; g < ng; ++g) {
-        int32_t pw = (cnt[g] + 3) & ~3;
-        if (pw > P.width[g * warps + w]) P.width[g * warps + w] = pw;
+      if (bank.on() && t % rq == 0) std::fill(ccnt.begin(), ccnt.end(), 0);
+      int32_t r = cta_rows[b * rows_per_cta + t];
+      if (r >= 0) {
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) {
+          const int32_t col = indices[j];
+          ++cnt[group_of[col]];
+          if (bank.on()) ++ccnt[group_of[col] * 8 + cls_of[col]];
+        }
+        for (int64_t g = 0; g < ng; ++g) {
+          int32_t pw = (cnt[g] + 3) & ~3;
+          if (pw > P.width[g * warps + w]) P.width[g * warps + w] = pw;
+        }
+      }
+      if (bank.on() && t % rq == rq - 1) {
+        for (int64_t g = 0; g < ng; ++g)
+          for (int c = 0; c < 8; ++c) {
+            int32_t pw = (ccnt[g * 8 + c] + 3) & ~3;
+            if (pw > P.width[g * warps + w]) P.width[g * warps + w] = pw;
+          }
       }
     }
   });
@@ -234,13 +348,13 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
   std::vector<double> worst(n_cta, 0.0);
   std::vector<int64_t> under(n_cta, 0);
   parallel_for(n_cta, n_threads, [&](int64_t b) {
+    if (err) return;
     const CtaPlan& P = plans[b];
     const int32_t* keys = key_tables + (int64_t)cta_table[b] * n_cols;
     const int64_t g0 = F->cta_group_ptr[b];
     for (size_t i = 0; i < P.foot.size(); ++i) F->group_map[cta_slot0[b] + i] = P.foot[i].col;
     const int64_t ng = P.gstart.empty() ? 0 : (int64_t)P.gstart.size() - 1;
     std::vector<std::pair<int32_t, int64_t>> ent;   // (key, csr position)
-    std::vector<int32_t> pos_in_group(ng);
     static thread_local std::vector<int32_t> slot_of, group_of;
     if ((int64_t)slot_of.size() < n_cols) { slot_of.assign(n_cols, 0); group_of.assign(n_cols, 0); }
     for (int64_t g = 0; g < ng; ++g)
@@ -250,49 +364,101 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
       }
     double wmax = 0.0;
     int64_t nunder = 0;
+    // entries of every (group, thread-row) in (key, CSR position) order
+    struct Ent { int32_t slot; int64_t j; };
+    std::vector<std::vector<Ent>> per(ng * rows_per_cta);
     for (int64_t t = 0; t < rows_per_cta; ++t) {
       int32_t r = cta_rows[b * rows_per_cta + t];
       if (r < 0) continue;
-      const int64_t w = t / rows_per_warp, rin = t % rows_per_warp;
       ent.clear();
       for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) ent.push_back({keys[indices[j]], j});
       std::stable_sort(ent.begin(), ent.end(),
                        [](const std::pair<int32_t, int64_t>& a,
                           const std::pair<int32_t, int64_t>& c) { return a.first < c.first; });
-      std::fill(pos_in_group.begin(), pos_in_group.end(), 0);
       for (auto& e : ent) {
         const int32_t col = indices[e.second];
-        const int64_t g = group_of[col];
-        const int64_t slot = slot_of[col];
-        int32_t n = pos_in_group[g]++;
-        int64_t gg = g0 + g;
-        int64_t at = F->slab_off[gg * warps + w] + ((int64_t)(n >> 2) * rows_per_warp + rin) * 4 + (n & 3);
-        F->slots[at] = (uint16_t)slot;
-        double v = values[e.second] * scale;   // exact power-of-two rescale
-        double back;
-        uint8_t* dst = F->values.data() + at * vbytes;
-        if (precision == XCT_DOUBLE) {
-          std::memcpy(dst, &v, 8);
-          back = v;
-        } else if (precision == XCT_SINGLE) {
-          float f = (float)v;
-          std::memcpy(dst, &f, 4);
-          back = (double)f;
-        } else {
-          uint16_t h = f64_to_f16(v);
-          std::memcpy(dst, &h, 2);
-          back = f16_to_f64(h);
+        per[(int64_t)group_of[col] * rows_per_cta + t].push_back({slot_of[col], e.second});
+      }
+    }
+    auto write = [&](int64_t gg, int64_t w, int64_t rin, int64_t n, int32_t slot, int64_t j) {
+      int64_t at = F->slab_off[gg * warps + w] + ((n >> 2) * rows_per_warp + rin) * 4 + (n & 3);
+      F->slots[at] = (uint16_t)slot;
+      if (j < 0) return;                       // padding: value stays 0
+      double v = values[j] * scale;           // exact power-of-two rescale
+      double back;
+      uint8_t* dst = F->values.data() + at * vbytes;
+      if (precision == XCT_DOUBLE) {
+        std::memcpy(dst, &v, 8);
+        back = v;
+      } else if (precision == XCT_SINGLE) {
+        float f = (float)v;
+        std::memcpy(dst, &f, 4);
+        back = (double)f;
+      } else {
+        uint16_t h = f64_to_f16(v);
+        std::memcpy(dst, &h, 2);
+        back = f16_to_f64(h);
+      }
+      if (v != 0.0) {
+        if (back == 0.0) ++nunder;
+        double rel = std::fabs(back - v) / std::fabs(v);
+        if (rel > wmax) wmax = rel;
+      }
+    };
+    Colorer colorer;
+    std::vector<int32_t> step_slot;
+    for (int64_t g = 0; g < ng; ++g) {
+      const int64_t gg = g0 + g;
+      for (int64_t w = 0; w < warps; ++w) {
+        const int64_t width = F->slab_width[gg * warps + w];
+        if (!bank.on()) {
+          for (int64_t rin = 0; rin < rows_per_warp; ++rin) {
+            const auto& L = per[g * rows_per_cta + w * rows_per_warp + rin];
+            for (size_t n = 0; n < L.size(); ++n) write(gg, w, rin, (int64_t)n, L[n].slot, L[n].j);
+          }
+          continue;
         }
-        if (v != 0.0) {
-          if (back == 0.0) ++nunder;
-          double rel = std::fabs(back - v) / std::fabs(v);
-          if (rel > wmax) wmax = rel;
+        for (int64_t q0 = 0; q0 < rows_per_warp; q0 += bank.rq) {
+          colorer.reset((int)bank.rq, 8, (int)width);
+          step_slot.assign(width, -1);
+          std::vector<std::pair<int64_t, int32_t>> owner;   // edge -> (rin, list index)
+          for (int64_t rr = 0; rr < bank.rq; ++rr) {
+            const auto& L = per[g * rows_per_cta + w * rows_per_warp + q0 + rr];
+            for (size_t n = 0; n < L.size(); ++n) {
+              if (!colorer.add((int)rr, bank.cls(L[n].slot))) {
+                std::lock_guard<std::mutex> lk(err_mu);
+                err = XCT_EINVAL;
+                err_msg = "format_build: bank schedule exceeded the slab width";
+                return;
+              }
+              owner.push_back({q0 + rr, (int32_t)n});
+            }
+          }
+          std::vector<char> used((size_t)bank.rq * width, 0);
+          for (size_t e = 0; e < owner.size(); ++e) {
+            const int64_t rin = owner[e].first;
+            const Ent& E = per[g * rows_per_cta + w * rows_per_warp + rin][owner[e].second];
+            const int64_t n = colorer.col[e];
+            write(gg, w, rin, n, E.slot, E.j);
+            used[(size_t)(rin - q0) * width + n] = 1;
+            if (step_slot[n] < 0) step_slot[n] = E.slot;
+          }
+          // idle lanes re-read a slot another lane of the quarter reads in the
+          // same step (broadcast, no extra bank traffic)
+          for (int64_t rr = 0; rr < bank.rq; ++rr)
+            for (int64_t n = 0; n < width; ++n)
+              if (!used[(size_t)rr * width + n] && step_slot[n] > 0)
+                write(gg, w, q0 + rr, n, step_slot[n], -1);
         }
       }
     }
     worst[b] = wmax;
     under[b] = nunder;
   });
+  if (err) {
+    delete F;
+    return xct::fail(err, err_msg);
+  }
 
   F->info.n_cta = n_cta;
   F->info.rows_per_cta = rows_per_cta;

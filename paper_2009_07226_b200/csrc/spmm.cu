@@ -10,10 +10,14 @@
 // Execution model (one CTA = one tile of rows, one F-chunk):
 //   for each load group of the tile:
 //     stage the group's input records x[elem][0:F] into shared memory with
-//       cp.async (16 B per lane, LDGSTS), one record = L 16-byte pieces;
-//     every lane of a warp owns 16 B (V slices) of one row's record and
-//       walks the (group, warp) slab: 4 entries per 128-bit streaming load,
-//       one 128-bit LDS per entry, V multiply-adds into registers;
+//       cp.async (16 B per lane, LDGSTS, double-buffered: the next group is
+//       staged while this one is consumed); a record is NP 16-byte pieces
+//       kept in NP bank-shifted planes;
+//     each row is owned by L lanes (L = 1 when the accumulators fit), each
+//       lane NPL = NP/L pieces; the lane walks its row in the (group, warp)
+//       slab 4 entries per 128-bit streaming load, with a kDepth-deep
+//       register ring of loads in flight, NPL 128-bit LDS and NPL*V
+//       multiply-adds per entry;
 //   epilogue writes the row's F outputs once.
 // Accumulation per row is sequential in stored order, so results are
 // deterministic and, with reference-stage keys, bit-identical to the
@@ -37,7 +41,8 @@ struct Params {
   const void* values;
   const uint4* x;
   int64_t n_in;
-  int32_t rows_per_cta, warps_per_cta, log2_lanes, n_cta;
+  int32_t rows_per_cta, warps_per_cta, log2_lanes, log2_pieces, n_cta;
+  int32_t plane_slots;      // slots per shared-memory plane (multiple of 8)
   // epilogue
   void* out;
   int64_t row_stride, chunk_stride;
@@ -46,25 +51,47 @@ struct Params {
   double* dot_partials;
 };
 
-__device__ __forceinline__ uint2 ld_stream_u2(const void* p) {
-  uint2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
-               : "=r"(v.x), "=r"(v.y) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  return v;
-}
+// ---- memory access helpers -------------------------------------------------
+// Entries stream through L2 once per F-chunk (evict_first); staged input
+// records are re-read by many tiles (evict_last).
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s), "l"(gmem));
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint2 ld_stream_u2(const void* p, uint64_t pol) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+               : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const void* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void cp_async16(uint32_t smem, const void* gmem, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
+               :: "r"(smem), "l"(gmem), "l"(pol));
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ float fhfma(unsigned short a, unsigned short b, float c) {
@@ -73,199 +100,287 @@ __device__ __forceinline__ float fhfma(unsigned short a, unsigned short b, float
   return d;
 }
 
-// ---- per-precision arithmetic ---------------------------------------------
+// ---- entry streams: 4 entries of one row per step -------------------------
+// slot fields hold the byte offset (slot * 16) of the record inside a plane.
+// half/mixed: one packed u32 per entry (offset << 16 | fp16 length)
+// single: u16 offsets + f32 lengths; double: u16 offsets + f64 lengths.
 
-template <int PREC> struct Acc;
+template <int PREC> struct Step;
 
-template <> struct Acc<XCT_MIXED> {          // fp16 storage, fp32 accumulate
-  static constexpr int V = 8;                // slices per lane (16 B of halves)
-  using Val4 = uint2;                        // 4 fp16 lengths
-  float a[8];
-  __device__ void zero() { for (int i = 0; i < 8; ++i) a[i] = 0.f; }
-  __device__ static Val4 load4(const void* base, int64_t idx) {
-    return ld_stream_u2((const uint16_t*)base + idx);
+template <> struct Step<XCT_MIXED> {
+  uint4 w;
+  __device__ void load(const uint16_t*, const void* v, int64_t idx, uint64_t pol) {
+    w = ld_stream_u4((const uint32_t*)v + idx, pol);
   }
-  __device__ static unsigned short pick(const Val4& v, int e) {
-    unsigned w = e < 2 ? v.x : v.y;
-    return (unsigned short)((e & 1) ? (w >> 16) : (w & 0xffff));
+  __device__ uint32_t word(int e) const { return e == 0 ? w.x : e == 1 ? w.y : e == 2 ? w.z : w.w; }
+  __device__ uint32_t off(int e) const { return word(e) >> 16; }
+  __device__ unsigned short val(int e) const { return (unsigned short)(word(e) & 0xffffu); }
+};
+template <> struct Step<XCT_HALF> : Step<XCT_MIXED> {};
+
+template <> struct Step<XCT_SINGLE> {
+  uint2 s;
+  uint4 v;
+  __device__ void load(const uint16_t* sl, const void* vv, int64_t idx, uint64_t pol) {
+    s = ld_stream_u2(sl + idx, pol);
+    v = ld_stream_u4((const float*)vv + idx, pol);
   }
-  __device__ void fma(const uint4& r, unsigned short len) {
-    const unsigned w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      a[2 * i] = fhfma((unsigned short)(w[i] & 0xffff), len, a[2 * i]);
-      a[2 * i + 1] = fhfma((unsigned short)(w[i] >> 16), len, a[2 * i + 1]);
-    }
+  __device__ uint32_t off(int e) const {
+    uint32_t q = e < 2 ? s.x : s.y;
+    return (e & 1) ? (q >> 16) : (q & 0xffffu);
   }
-  __device__ void result(float scale, float* out) const {
-    for (int i = 0; i < 8; ++i) out[i] = __half2float(__float2half_rn(a[i] * scale));
+  __device__ float val(int e) const {
+    return __uint_as_float(e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w);
   }
 };
 
-template <> struct Acc<XCT_HALF> {           // fp16 storage and accumulate
+template <> struct Step<XCT_DOUBLE> {
+  uint2 s;
+  uint4 lo, hi;
+  __device__ void load(const uint16_t* sl, const void* vv, int64_t idx, uint64_t pol) {
+    s = ld_stream_u2(sl + idx, pol);
+    const double* p = (const double*)vv + idx;
+    lo = ld_stream_u4(p, pol);
+    hi = ld_stream_u4(p + 2, pol);
+  }
+  __device__ uint32_t off(int e) const {
+    uint32_t q = e < 2 ? s.x : s.y;
+    return (e & 1) ? (q >> 16) : (q & 0xffffu);
+  }
+  __device__ double val(int e) const {
+    const uint4& q = e < 2 ? lo : hi;
+    unsigned long long b = (e & 1) ? ((unsigned long long)q.w << 32 | q.z)
+                                   : ((unsigned long long)q.y << 32 | q.x);
+    return __longlong_as_double((long long)b);
+  }
+};
+
+// ---- per-precision accumulators over NPL 16-byte pieces -----------------------
+
+template <int PREC, int NPL> struct Acc;
+
+template <int NPL> struct Acc<XCT_MIXED, NPL> {   // fp16 storage, fp32 accumulate
+  static constexpr int V = 8;                      // slices per 16-byte piece
+  float a[8 * NPL];
+  __device__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 8 * NPL; ++i) a[i] = 0.f;
+  }
+  __device__ void fma(int q, const uint4& r, unsigned short len) {
+    const unsigned w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a[8 * q + 2 * i] = fhfma((unsigned short)(w[i] & 0xffff), len, a[8 * q + 2 * i]);
+      a[8 * q + 2 * i + 1] = fhfma((unsigned short)(w[i] >> 16), len, a[8 * q + 2 * i + 1]);
+    }
+  }
+  __device__ float out(int i, float scale) const {
+    return __half2float(__float2half_rn(a[i] * scale));
+  }
+};
+
+template <int NPL> struct Acc<XCT_HALF, NPL> {     // fp16 storage and accumulate
   static constexpr int V = 8;
-  using Val4 = uint2;
-  __half2 a[4];
-  __device__ void zero() { for (int i = 0; i < 4; ++i) a[i] = __float2half2_rn(0.f); }
-  __device__ static Val4 load4(const void* base, int64_t idx) {
-    return ld_stream_u2((const uint16_t*)base + idx);
+  __half2 a[4 * NPL];
+  __device__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 4 * NPL; ++i) a[i] = __float2half2_rn(0.f);
   }
-  __device__ static unsigned short pick(const Val4& v, int e) {
-    unsigned w = e < 2 ? v.x : v.y;
-    return (unsigned short)((e & 1) ? (w >> 16) : (w & 0xffff));
-  }
-  __device__ void fma(const uint4& r, unsigned short len) {
+  __device__ void fma(int q, const uint4& r, unsigned short len) {
     __half h = __ushort_as_half(len);
     __half2 l2 = __halves2half2(h, h);
     const unsigned w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       __half2 x = *reinterpret_cast<const __half2*>(&w[i]);
-      a[i] = __hadd2_rn(a[i], __hmul2_rn(x, l2));   // two roundings, as numpy f16
+      a[4 * q + i] = __hadd2_rn(a[4 * q + i], __hmul2_rn(x, l2));  // numpy f16: 2 roundings
     }
   }
-  __device__ void result(float scale, float* out) const {
+  __device__ float out(int i, float scale) const {
     __half hs = __float2half_rn(scale);
-    for (int i = 0; i < 4; ++i) {
-      __half2 v = __hmul2_rn(a[i], __halves2half2(hs, hs));
-      out[2 * i] = __low2float(v);
-      out[2 * i + 1] = __high2float(v);
-    }
+    __half2 v = __hmul2_rn(a[i >> 1], __halves2half2(hs, hs));
+    return (i & 1) ? __high2float(v) : __low2float(v);
   }
 };
 
-template <> struct Acc<XCT_SINGLE> {         // fp32 storage and accumulate
+template <int NPL> struct Acc<XCT_SINGLE, NPL> {   // fp32 storage and accumulate
   static constexpr int V = 4;
-  using Val4 = uint4;
-  float a[4];
-  __device__ void zero() { for (int i = 0; i < 4; ++i) a[i] = 0.f; }
-  __device__ static Val4 load4(const void* base, int64_t idx) {
-    return ld_stream_u4((const float*)base + idx);
+  float a[4 * NPL];
+  __device__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 4 * NPL; ++i) a[i] = 0.f;
   }
-  __device__ static float pick(const Val4& v, int e) {
-    unsigned w = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
-    return __uint_as_float(w);
-  }
-  __device__ void fma(const uint4& r, float len) {
+  __device__ void fma(int q, const uint4& r, float len) {
     const unsigned w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = __fadd_rn(a[i], __fmul_rn(__uint_as_float(w[i]), len));
+    for (int i = 0; i < 4; ++i)
+      a[4 * q + i] = __fadd_rn(a[4 * q + i], __fmul_rn(__uint_as_float(w[i]), len));
   }
-  __device__ void result(float scale, float* out) const {
-    for (int i = 0; i < 4; ++i) out[i] = a[i] * scale;
-  }
+  __device__ float out(int i, float scale) const { return a[i] * scale; }
 };
 
-template <> struct Acc<XCT_DOUBLE> {         // fp64 storage and accumulate
+template <int NPL> struct Acc<XCT_DOUBLE, NPL> {   // fp64 storage and accumulate
   static constexpr int V = 2;
-  struct Val4 { uint4 lo, hi; };
-  double a[2];
-  __device__ void zero() { a[0] = a[1] = 0.0; }
-  __device__ static Val4 load4(const void* base, int64_t idx) {
-    const double* p = (const double*)base + idx;
-    return {ld_stream_u4(p), ld_stream_u4(p + 2)};
+  double a[2 * NPL];
+  __device__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 2 * NPL; ++i) a[i] = 0.0;
   }
-  __device__ static double pick(const Val4& v, int e) {
-    const uint4& q = e < 2 ? v.lo : v.hi;
-    unsigned long long bits = (e & 1) ? ((unsigned long long)q.w << 32 | q.z)
-                                      : ((unsigned long long)q.y << 32 | q.x);
-    return __longlong_as_double((long long)bits);
-  }
-  __device__ void fma(const uint4& r, double len) {
+  __device__ void fma(int q, const uint4& r, double len) {
     double x0 = __longlong_as_double((long long)((unsigned long long)r.y << 32 | r.x));
     double x1 = __longlong_as_double((long long)((unsigned long long)r.w << 32 | r.z));
-    a[0] = __dadd_rn(a[0], __dmul_rn(x0, len));
-    a[1] = __dadd_rn(a[1], __dmul_rn(x1, len));
+    a[2 * q] = __dadd_rn(a[2 * q], __dmul_rn(x0, len));
+    a[2 * q + 1] = __dadd_rn(a[2 * q + 1], __dmul_rn(x1, len));
   }
-  __device__ void result(double scale, double* out) const {
-    out[0] = a[0] * scale;
-    out[1] = a[1] * scale;
-  }
+  __device__ double out(int i, double scale) const { return a[i] * scale; }
 };
 
-template <int PREC>
+// Shared-memory stage: a record's NP 16-byte pieces live in NP planes of
+// plane_slots records each.  Plane p is shifted by (8/NP)*p bank quads
+// (p mod 8 when NP > 8), so the L lanes of a row never collide and rows
+// collide only when their slots agree mod 8/L (the builder's bank classes).
+__device__ __forceinline__ uint32_t plane_base(int p, int lp, int plane_slots) {
+  const int shift = lp <= 3 ? ((p << (3 - lp)) & 7) : (p & 7);
+  return (uint32_t)p * (uint32_t)plane_slots * 16u + 16u * (uint32_t)shift;
+}
+__device__ __forceinline__ uint32_t buffer_bytes(int lp, int plane_slots) {
+  return ((uint32_t)plane_slots << (lp + 4)) + 128u;
+}
+
+constexpr int kDepth = 4;     // entry steps in flight per lane (register ring)
+constexpr int kFillUnroll = 4;
+
+// Stage the records of load group g into the buffer at shared address dst.
+// Piece-interleaved (full 32-byte sectors per pair of lanes); the map is
+// read kFillUnroll ahead so the loads are independent.
+__device__ __forceinline__ void stage_fill(const Params& p, const uint4* xb, uint32_t dst, int g,
+                                           int lp, uint64_t pol) {
+  const int64_t m0 = p.group_map_ptr[g];
+  const int pieces = (int)(p.group_map_ptr[g + 1] - m0) << lp;
+  const int NP = 1 << lp;
+  for (int i0 = threadIdx.x; i0 < pieces; i0 += blockDim.x * kFillUnroll) {
+    int32_t e[kFillUnroll];
+#pragma unroll
+    for (int u = 0; u < kFillUnroll; ++u) {
+      const int i = i0 + u * blockDim.x;
+      e[u] = i < pieces ? __ldg(p.group_map + m0 + (i >> lp)) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kFillUnroll; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < pieces) {
+        const int s = i >> lp, q = i & (NP - 1);
+        cp_async16(dst + plane_base(q, lp, p.plane_slots) + ((uint32_t)s << 4),
+                   xb + ((int64_t)e[u] << lp) + q, pol);
+      }
+    }
+  }
+}
+
+template <int PREC, int NPL, typename A, typename St>
+__device__ __forceinline__ void consume(A& acc, const St& cur, const uint32_t (&pb)[NPL]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t off = cur.off(e);
+    const auto len = cur.val(e);
+#pragma unroll
+    for (int qq = 0; qq < NPL; ++qq) acc.fma(qq, lds128(pb[qq] + off), len);
+  }
+}
+
+template <int PREC, int NPL>
 __global__ void __launch_bounds__(1024) spmm_staged_kernel(const Params p) {
-  using A = Acc<PREC>;
+  using A = Acc<PREC, NPL>;
+  using St = Step<PREC>;
   constexpr int V = A::V;
   extern __shared__ uint4 stage[];
   const int b = blockIdx.x;
   const int chunk = blockIdx.y;
-  const int lg = p.log2_lanes;
-  const int L = 1 << lg;
+  const int lg = p.log2_lanes;               // lanes per row = 1 << lg
+  const int lp = p.log2_pieces;              // 16-byte pieces per record = 1 << lp
   const int rpw = 32 >> lg;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rin = lane >> lg, sub = lane & (L - 1);
-  const int trow = warp * rpw + rin;
-  const int row = p.cta_rows[(int64_t)b * p.rows_per_cta + trow];
-  const uint4* xb = p.x + (int64_t)chunk * p.n_in * L;
+  const int rin = lane >> lg, sub = lane & ((1 << lg) - 1);
+  const int row = p.cta_rows[(int64_t)b * p.rows_per_cta + warp * rpw + rin];
+  const uint4* xb = p.x + (int64_t)chunk * p.n_in * (1 << lp);
+  const uint64_t pol_x = policy_evict_last(), pol_e = policy_evict_first();
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(stage);
+  const uint32_t bb = buffer_bytes(lp, p.plane_slots);
+  uint32_t pbase[NPL];
+#pragma unroll
+  for (int qq = 0; qq < NPL; ++qq) pbase[qq] = plane_base(sub * NPL + qq, lp, p.plane_slots);
 
   A acc;
   acc.zero();
   const int g0 = p.cta_group_ptr[b], g1 = p.cta_group_ptr[b + 1];
+  // two stage buffers: group g+1 is staged while group g is consumed
+  if (g0 < g1) stage_fill(p, xb, s0, g0, lp, pol_x);
+  cp_async_commit();
   for (int g = g0; g < g1; ++g) {
-    const int64_t m0 = p.group_map_ptr[g];
-    const int ns = (int)(p.group_map_ptr[g + 1] - m0);
-    const int pieces = ns << lg;
-    for (int i = threadIdx.x; i < pieces; i += blockDim.x) {
-      const int32_t e = p.group_map[m0 + (i >> lg)];
-      cp_async16(&stage[i], xb + (int64_t)e * L + (i & (L - 1)));
-    }
+    const uint32_t cur_buf = s0 + (((g - g0) & 1) ? bb : 0u);
     cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();                     // fill(g) visible; everyone done with g-1
+    if (g + 1 < g1) stage_fill(p, xb, s0 + (((g - g0) & 1) ? 0u : bb), g + 1, lp, pol_x);
+    cp_async_commit();
 
+    uint32_t pb[NPL];
+#pragma unroll
+    for (int qq = 0; qq < NPL; ++qq) pb[qq] = cur_buf + pbase[qq];
     const int64_t off = p.slab_off[(int64_t)g * p.warps_per_cta + warp];
     const int n4 = p.slab_width[(int64_t)g * p.warps_per_cta + warp] >> 2;
-    const uint16_t* sl = p.slots + off;
-    if (n4 > 0) {
-      int64_t idx = (int64_t)rin * 4;
-      uint2 s_next = ld_stream_u2(sl + idx);
-      typename A::Val4 v_next = A::load4(p.values, off + idx);
-      for (int k = 0; k < n4; ++k) {
-        const uint2 s4 = s_next;
-        const typename A::Val4 v4 = v_next;
-        if (k + 1 < n4) {
-          idx += (int64_t)rpw * 4;
-          s_next = ld_stream_u2(sl + idx);
-          v_next = A::load4(p.values, off + idx);
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const unsigned w = e < 2 ? s4.x : s4.y;
-          const unsigned slot = (e & 1) ? (w >> 16) : (w & 0xffffu);
-          const uint4 r = stage[(slot << lg) + sub];
-          acc.fma(r, A::pick(v4, e));
-        }
-      }
+    const int64_t step = (int64_t)rpw * 4;
+    int64_t at = off + (int64_t)rin * 4;
+    // ring of kDepth steps; a slot is refilled right after it is consumed.
+    // The entry arrays are padded so prefetching past a slab end is safe.
+    St r0, r1, r2, r3;
+    r0.load(p.slots, p.values, at, pol_e);
+    r1.load(p.slots, p.values, at + step, pol_e);
+    r2.load(p.slots, p.values, at + 2 * step, pol_e);
+    r3.load(p.slots, p.values, at + 3 * step, pol_e);
+    at += 4 * step;
+    for (int k = 0; k < n4; k += kDepth) {
+      consume<PREC, NPL>(acc, r0, pb);
+      r0.load(p.slots, p.values, at, pol_e);
+      if (k + 1 >= n4) break;
+      consume<PREC, NPL>(acc, r1, pb);
+      r1.load(p.slots, p.values, at + step, pol_e);
+      if (k + 2 >= n4) break;
+      consume<PREC, NPL>(acc, r2, pb);
+      r2.load(p.slots, p.values, at + 2 * step, pol_e);
+      if (k + 3 >= n4) break;
+      consume<PREC, NPL>(acc, r3, pb);
+      r3.load(p.slots, p.values, at + 3 * step, pol_e);
+      at += 4 * step;
     }
-    __syncthreads();
   }
+  cp_async_wait_all();
 
   // ---- epilogue -----------------------------------------------------------
   double sq = 0.0;
   if (row >= 0) {
-    const int j0 = sub * V;
+    const int j0 = sub * NPL * V;
     if constexpr (PREC == XCT_DOUBLE) {
-      double o[V];
-      acc.result(ldexp(1.0, -p.scale_exp), o);
+      const double sc = ldexp(1.0, -p.scale_exp);
       const double f = p.factors ? p.factors[chunk] : 1.0;
       double* out = (double*)p.out + (int64_t)row * p.row_stride + (int64_t)chunk * p.chunk_stride;
-      for (int i = 0; i < V; ++i) {
-        int j = j0 + i;
+#pragma unroll
+      for (int i = 0; i < NPL * V; ++i) {
+        const int j = j0 + i;
         if (j < p.ffactor && chunk * p.ffactor + j < p.valid_cols) {
-          double v = o[i] * f;
+          const double v = acc.out(i, sc) * f;
           out[j] = v;
           sq += v * v;
         }
       }
     } else {
-      float o[V];
-      acc.result(ldexpf(1.0f, -p.scale_exp), o);
+      const float sc = ldexpf(1.0f, -p.scale_exp);
       const float f = p.factors ? (float)p.factors[chunk] : 1.0f;
       float* out = (float*)p.out + (int64_t)row * p.row_stride + (int64_t)chunk * p.chunk_stride;
-      for (int i = 0; i < V; ++i) {
-        int j = j0 + i;
+#pragma unroll
+      for (int i = 0; i < NPL * V; ++i) {
+        const int j = j0 + i;
         if (j < p.ffactor && chunk * p.ffactor + j < p.valid_cols) {
-          float v = o[i] * f;
+          const float v = acc.out(i, sc) * f;
           out[j] = v;
           sq += (double)v * (double)v;
         }
@@ -285,19 +400,31 @@ __global__ void __launch_bounds__(1024) spmm_staged_kernel(const Params p) {
   }
 }
 
-template <int PREC>
+template <int PREC, int NPL>
 int launch(const Params& p, int64_t n_chunks, int threads, int64_t smem, cudaStream_t s) {
   static int configured = -1;
-  if (configured != (int)smem) {
-    cudaError_t e = cudaFuncSetAttribute(spmm_staged_kernel<PREC>,
+  if (configured < (int)smem) {
+    cudaError_t e = cudaFuncSetAttribute(spmm_staged_kernel<PREC, NPL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return xct::fail(XCT_ECUDA, std::string("spmm smem attribute: ") + cudaGetErrorString(e));
+    if (e != cudaSuccess)
+      return xct::fail(XCT_ECUDA, std::string("spmm smem attribute: ") + cudaGetErrorString(e));
     configured = (int)smem;
   }
   dim3 grid((unsigned)p.n_cta, (unsigned)n_chunks);
-  spmm_staged_kernel<PREC><<<grid, threads, smem, s>>>(p);
+  spmm_staged_kernel<PREC, NPL><<<grid, threads, smem, s>>>(p);
   XCT_CUDA_CHECK_LAUNCH("spmm_staged");
   return XCT_OK;
+}
+
+template <int PREC>
+int launch_npl(const Params& p, int npl, int64_t n_chunks, int threads, int64_t smem,
+               cudaStream_t s) {
+  switch (npl) {
+    case 1: return launch<PREC, 1>(p, n_chunks, threads, smem, s);
+    case 2: return launch<PREC, 2>(p, n_chunks, threads, smem, s);
+    case 4: return launch<PREC, 4>(p, n_chunks, threads, smem, s);
+    default: return xct::fail(XCT_EINVAL, "spmm: pieces per lane must be 1, 2 or 4");
+  }
 }
 
 }  // namespace
@@ -308,21 +435,28 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   if (!a || !ep || !d_x || !ep->d_out) return xct::fail(XCT_EINVAL, "spmm: null argument");
   if (precision < 0 || precision > 3) return xct::fail(XCT_EINVAL, "spmm: bad precision");
   if (ep->accumulate) return xct::fail(XCT_EINVAL, "spmm: accumulate mode is reserved");
+  const bool packed = precision == XCT_HALF || precision == XCT_MIXED;
+  if (!a->d_values || (!packed && !a->d_slots))
+    return xct::fail(XCT_EINVAL, "spmm: missing entry arrays");
   const int vbytes = precision == XCT_DOUBLE ? 8 : precision == XCT_SINGLE ? 4 : 2;
   const int64_t rec = (int64_t)f_dev * vbytes;
   if (rec < 16 || rec > 512 || (rec & (rec - 1)))
     return xct::fail(XCT_EINVAL, "spmm: f_dev*elem_bytes must be a power of two in [16, 512]");
-  int lg = 0;
-  while ((16 << lg) < rec) ++lg;
-  if (a->rows_per_warp != (32 >> lg))
-    return xct::fail(XCT_EINVAL, "spmm: format rows_per_warp does not match f_dev/precision");
+  int lp = 0;
+  while ((16 << lp) < rec) ++lp;                      // pieces per record = 1 << lp
+  int lg = 0;                                         // lanes per row = 1 << lg
+  while ((32 >> lg) > a->rows_per_warp && lg < 5) ++lg;
+  if ((32 >> lg) != a->rows_per_warp || lg > lp)
+    return xct::fail(XCT_EINVAL, "spmm: rows_per_warp must be 32 / lanes with lanes <= pieces");
+  const int npl = 1 << (lp - lg);
   if (a->n_cta == 0 || n_chunks == 0) return XCT_OK;
   if (n_chunks > 65535) return xct::fail(XCT_EINVAL, "spmm: too many chunks for one launch");
   const int threads = (int)(a->warps_per_cta * 32);
   if (threads < 32 || threads > 1024) return xct::fail(XCT_EINVAL, "spmm: CTA must have 1..32 warps");
-  int64_t need = a->max_group_slots * rec;
+  const int64_t plane_slots = (a->max_group_slots + 7) & ~(int64_t)7;
+  if (plane_slots * 16 > 65536) return xct::fail(XCT_ESTAGE, "spmm: plane offsets exceed 16 bits");
+  const int64_t need = 2 * ((plane_slots << (lp + 4)) + 128);   // double-buffered stage
   if (smem_bytes < need) smem_bytes = need;
-  if (smem_bytes < 16) smem_bytes = 16;
   if (smem_bytes > 227 * 1024) return xct::fail(XCT_ESTAGE, "spmm: load group exceeds shared memory");
 
   Params p;
@@ -339,7 +473,9 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   p.rows_per_cta = (int32_t)a->rows_per_cta;
   p.warps_per_cta = (int32_t)a->warps_per_cta;
   p.log2_lanes = lg;
+  p.log2_pieces = lp;
   p.n_cta = (int32_t)a->n_cta;
+  p.plane_slots = (int32_t)plane_slots;
   p.out = ep->d_out;
   p.row_stride = ep->row_stride;
   p.chunk_stride = ep->chunk_stride;
@@ -350,10 +486,10 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   p.dot_partials = ep->d_dot_partials;
   cudaStream_t s = (cudaStream_t)stream;
   switch (precision) {
-    case XCT_DOUBLE: return launch<XCT_DOUBLE>(p, n_chunks, threads, smem_bytes, s);
-    case XCT_SINGLE: return launch<XCT_SINGLE>(p, n_chunks, threads, smem_bytes, s);
-    case XCT_HALF: return launch<XCT_HALF>(p, n_chunks, threads, smem_bytes, s);
-    default: return launch<XCT_MIXED>(p, n_chunks, threads, smem_bytes, s);
+    case XCT_DOUBLE: return launch_npl<XCT_DOUBLE>(p, npl, n_chunks, threads, smem_bytes, s);
+    case XCT_SINGLE: return launch_npl<XCT_SINGLE>(p, npl, n_chunks, threads, smem_bytes, s);
+    case XCT_HALF: return launch_npl<XCT_HALF>(p, npl, n_chunks, threads, smem_bytes, s);
+    default: return launch_npl<XCT_MIXED>(p, npl, n_chunks, threads, smem_bytes, s);
   }
 }
 

@@ -46,6 +46,7 @@ WARP_WIDTH = 32
 DEFAULT_STAGE_CAPACITY = 96 * 1024      # src/matrixstore.py:44
 SAFE_MAX = 60000.0                      # src/matrixstore.py:46
 SMEM_BUDGET = 96 * 1024                 # per CTA: two resident CTAs per SM
+SMEM_MAX = 224 * 1024                   # opt-in maximum per CTA on sm_100a
 
 _STORE = {"double": np.float64, "single": np.float32, "half": np.float16, "mixed": np.float16}
 _COMPUTE = {"double": np.float64, "single": np.float32, "half": np.float16, "mixed": np.float32}
@@ -80,8 +81,12 @@ def f_dev_for(ffactor: int, precision: str) -> int:
     return rec // eb
 
 
-def lanes_for(ffactor: int, precision: str) -> int:
-    return f_dev_for(ffactor, precision) * element_bytes(precision) // 16
+def lanes_for(ffactor: int, precision: str, pieces_per_lane: int = 2) -> int:
+    """Lanes sharing one row in K6: a record is f_dev*elem_bytes/16 pieces of
+    16 bytes and every lane accumulates `pieces_per_lane` of them (2 keeps the
+    accumulators + a 4-deep load ring within 64 registers)."""
+    pieces = f_dev_for(ffactor, precision) * element_bytes(precision) // 16
+    return max(1, pieces // pieces_per_lane)
 
 
 def half_rescale_exponent(values) -> int:
@@ -342,7 +347,7 @@ class DeviceSide:
 def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndarray,
                       n_rows: int, n_cols: int, plan: Plan, precision: str, ffactor: int,
                       value_scale_exp: int, smem_budget: int = SMEM_BUDGET,
-                      dev=None) -> DeviceSide:
+                      dev=None, schedule: bool = False) -> DeviceSide:
     """Build the staged format on the host (libxct_b200 K5) and upload it."""
     import torch
     from .geometry import device
@@ -350,7 +355,8 @@ def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndar
     dev = dev or device()
     f_dev = f_dev_for(ffactor, precision)
     rec = f_dev * element_bytes(precision)
-    capacity = min(65536, max(1, smem_budget // rec))
+    # the kernel double-buffers the stage: two groups of `capacity` records
+    capacity = min(65536, max(1, smem_budget // (2 * rec)))
     rows = np.ascontiguousarray(plan.cta_rows, np.int32)
     keys = np.ascontiguousarray(plan.key_tables, np.int32)
     ctab = np.ascontiguousarray(plan.cta_table, np.int32)
@@ -359,10 +365,13 @@ def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndar
     vals = np.ascontiguousarray(values, np.float64)
     handle = C.c_void_p()
     L = _lib.lib()
+    lp = (rec // 16).bit_length() - 1
+    lg = (32 // plan.rows_per_warp).bit_length() - 1
     st = L.xct_format_build(n_rows, n_cols, ip.ctypes.data, ix.ctypes.data, vals.ctypes.data,
                             rows.shape[0], rows.shape[1], plan.rows_per_warp,
                             rows.ctypes.data, keys.ctypes.data, ctab.ctypes.data, capacity,
-                            _lib.PREC_CODE[precision], int(value_scale_exp), _lib.n_threads(),
+                            _lib.PREC_CODE[precision], int(value_scale_exp),
+                            lp if schedule else -1, lg if schedule else -1, _lib.n_threads(),
                             C.byref(handle))
     _lib.check(st, "xct_format_build")
     try:
@@ -382,6 +391,19 @@ def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndar
                    "xct_format_export")
     finally:
         L.xct_format_free(handle)
+    # K6 addresses a staged record by its byte offset inside a plane
+    plane_slots = -(-int(info.max_group_slots) // 8) * 8
+    if plane_slots * 16 > 65536:
+        raise StageSplitRequired("load group too large for 16-bit plane offsets")
+    h["slots"] = (h["slots"].astype(np.uint32) << 4).astype(np.uint16)
+    if precision in ("half", "mixed"):
+        # one 32-bit word per entry: byte offset << 16 | fp16 length
+        h["values"] = (h["slots"].astype(np.uint32) << 16) | h["values"].view(np.uint16)
+        h["values"] = h["values"].view(np.int32)
+        h["slots"] = np.zeros(1, np.uint16)
+    # the kernel's load ring reads up to 4 steps (x 32 rows x 4) past a slab
+    for k in ("slots", "values"):
+        h[k] = np.concatenate([h[k], np.zeros(1024, h[k].dtype)])
     t = {k: torch.from_numpy(v.view(np.int16) if v.dtype == np.uint16 else v).to(dev)
          for k, v in h.items()}
     t["cta_rows"] = torch.from_numpy(rows.reshape(-1)).to(dev)
@@ -400,5 +422,5 @@ def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndar
     s.d_slots = t["slots"].data_ptr()
     s.d_values = t["values"].data_ptr()
     side.staged = s
-    side.smem_bytes = int(max(16, info.max_group_slots * rec))
+    side.smem_bytes = int(2 * (plane_slots * rec + 128))
     return side

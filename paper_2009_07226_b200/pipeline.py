@@ -31,7 +31,7 @@ from .matrixstore import NormalizationState
 
 __all__ = ["SystemConfig", "AssembledSystem", "assemble", "assemble_from_matrix", "ORDERS"]
 
-ORDERS = ("native", "reference")
+ORDERS = ("native", "traversal", "reference")
 
 
 @dataclass(frozen=True)
@@ -39,9 +39,14 @@ class SystemConfig:
     """Parallelization and precision knobs (src/pipeline.py:26-47).
 
     Added for the B200 build (defaults keep the reference's meaning):
-      order          "native": image-band / view-range staging (traversal
-                     order per ray, ray-id order per voxel); "reference":
-                     the reference's stage order, bit-identical results.
+      order          "native": image-band / view-range staging with the
+                     bank-conflict-free step schedule (sums equal the
+                     reference's to rounding); "traversal": the same staging
+                     keeping traversal order per ray and ray-id order per
+                     voxel (bit-identical to the reference run with
+                     stage_capacity_bytes=None, block_partitions=1);
+                     "reference": the reference's stage order, bit-identical
+                     to the reference's default configuration.
       warps_per_cta  CTA size of the staged SpMM.
       smem_budget    shared-memory bytes per CTA for one load group.
     ``topology`` and ``comm_strategy`` are accepted for API compatibility;
@@ -154,12 +159,24 @@ class AssembledSystem:
             return matrixstore.adjoint_plan(g.num_angles, g.grid_n, rw, cfg.warps_per_cta)
         return matrixstore.row_block_plan(n_rows, n_cols, rw, cfg.warps_per_cta)
 
+    def _budget(self, plan) -> int:
+        """Shared memory per CTA: the configured budget, raised for reference
+        staging so one whole reference stage fits a (double-buffered) group."""
+        cfg = self.config
+        if plan.kind != "reference" or cfg.stage_capacity_bytes is None:
+            return cfg.smem_budget
+        rec = matrixstore.f_dev_for(cfg.ffactor, cfg.precision) * \
+            matrixstore.element_bytes(cfg.precision)
+        cap = cfg.stage_capacity_bytes // (matrixstore.element_bytes(cfg.precision) * cfg.ffactor)
+        return max(cfg.smem_budget, min(2 * cap * rec, matrixstore.SMEM_MAX))
+
     def _single_side(self, ip, ix, v, n_rows, n_cols, kind) -> _Side:
         cfg = self.config
         plan = self._plan(ip, ix, n_rows, n_cols, kind)
         blk = matrixstore.build_device_side(ip, ix, v, n_rows, n_cols, plan, cfg.precision,
                                             cfg.ffactor, self.value_scale_exp,
-                                            cfg.smem_budget, self.device)
+                                            self._budget(plan), self.device,
+                                            schedule=cfg.order == "native")
         ident = np.arange(n_rows)
         return _Side([blk], [None], [None], [ident], n_cols, n_rows)
 
@@ -179,7 +196,7 @@ class AssembledSystem:
                                               cfg.precision, rw, cfg.warps_per_cta)
             return matrixstore.build_device_side(bip, bix, bv, nr, nc, plan, cfg.precision,
                                                  cfg.ffactor, self.value_scale_exp,
-                                                 cfg.smem_budget, self.device)
+                                                 self._budget(plan), self.device)
 
         f_blocks, f_fp = [], []
         for sub in tomo:         # A[:, owned cols] over the rays it touches

@@ -38,10 +38,12 @@ def test_error_path_reports_message():
     assert b"angle" in lib.xct_last_error()
 
 
-def export(ip, ix, v, n_rows, n_cols, plan, prec, ff, exp=0, budget=96 * 1024):
+def export(ip, ix, v, n_rows, n_cols, plan, prec, ff, exp=0, budget=96 * 1024, schedule=False):
     f_dev = matrixstore.f_dev_for(ff, prec)
     rec = f_dev * matrixstore.element_bytes(prec)
-    cap = min(65536, budget // rec)
+    cap = min(65536, budget // (2 * rec))
+    lp = (rec // 16).bit_length() - 1
+    lg = (32 // plan.rows_per_warp).bit_length() - 1
     h = C.c_void_p()
     L = _lib.lib()
     rows = np.ascontiguousarray(plan.cta_rows, np.int32)
@@ -49,7 +51,8 @@ def export(ip, ix, v, n_rows, n_cols, plan, prec, ff, exp=0, budget=96 * 1024):
                             rows.shape[0], rows.shape[1], plan.rows_per_warp, rows.ctypes.data,
                             np.ascontiguousarray(plan.key_tables, np.int32).ctypes.data,
                             np.ascontiguousarray(plan.cta_table, np.int32).ctypes.data, cap,
-                            _lib.PREC_CODE[prec], exp, 4, C.byref(h))
+                            _lib.PREC_CODE[prec], exp, lp if schedule else -1,
+                            lg if schedule else -1, 4, C.byref(h))
     _lib.check(st, "build")
     info = _lib.FormatInfo()
     L.xct_format_get_info(h, C.byref(info))
@@ -99,7 +102,7 @@ def test_format_builder_native_and_reference_orders(prec):
     plan = matrixstore.assign_forward_regimes(
         matrixstore.forward_plan(g.num_angles, g.n, rw, 4), g.angles, g.n)
     info, a, rows, _ = export(ip, ix, v, A.num_rows, A.num_cols, plan, prec, 4, exp,
-                              budget=2048)
+                              budget=4096)
     assert info.n_groups > info.n_cta          # several load groups per tile
     seqs = replay(info, a, rows, A.num_rows)
     sd = matrixstore.storage_dtype(prec)
@@ -126,13 +129,13 @@ def test_format_builder_adjoint_ray_order_and_capacity_error():
     ip, ix, v = T.indptr, T.indices.astype(np.int32), T.values
     plan = matrixstore.adjoint_plan(g.num_angles, g.n, 8, 4)
     info, a, rows, _ = export(ip, ix, v, T.num_rows, T.num_cols, plan, "single", 16,
-                              budget=64 * 64)
+                              budget=2 * 64 * 64)
     seqs = replay(info, a, rows, T.num_rows)
     for r in range(T.num_rows):
         s, e = ip[r], ip[r + 1]
         assert [c for c, _ in seqs[r]] == ix[s:e].tolist()       # ascending ray id
     with pytest.raises(matrixstore.StageSplitRequired):
-        export(ip, ix, v, T.num_rows, T.num_cols, plan, "single", 16, budget=64 * 4)
+        export(ip, ix, v, T.num_rows, T.num_cols, plan, "single", 16, budget=2 * 64 * 4)
 
 
 def test_csr_transpose_is_the_reference_transpose():
@@ -159,3 +162,50 @@ def test_f64_to_f16_matches_numpy():
     seqs = replay(info, a, rows, len(vals))
     got = np.array([seqs[r][0][1] if seqs[r] else 0.0 for r in range(len(vals))])
     assert np.array_equal(got, vals.astype(np.float16).astype(np.float64))
+
+
+@pytest.mark.parametrize("prec", ["single", "mixed"])
+@pytest.mark.parametrize("side", ["forward", "adjoint"])
+def test_bank_conflict_free_schedule(prec, side):
+    """Scheduled slabs hold every row's entries exactly once (as a multiset)
+    and no two rows of a quarter-warp read the same bank class in a step."""
+    g = O.make_geom(40, 1, 32)
+    A = O.system_matrix(g)
+    ip, ix, v = A.indptr, A.indices.astype(np.int32), A.values
+    n_rows, n_cols = A.num_rows, A.num_cols
+    rw = 32 // matrixstore.lanes_for(16, prec)
+    if side == "adjoint":
+        T = O.transpose_block(O.whole_block(A))
+        ip, ix, v = T.indptr, T.indices.astype(np.int32), T.values
+        n_rows, n_cols = n_cols, n_rows
+        plan = matrixstore.adjoint_plan(g.num_angles, g.n, rw, 8)
+    else:
+        plan = matrixstore.assign_forward_regimes(
+            matrixstore.forward_plan(g.num_angles, g.n, rw, 8), g.angles, g.n)
+    info, a, rows, _ = export(ip, ix, v, n_rows, n_cols, plan, prec, 16, schedule=True)
+    seqs = replay(info, a, rows, n_rows)
+    sd = matrixstore.storage_dtype(prec)
+    for r in range(n_rows):
+        s_, e_ = ip[r], ip[r + 1]
+        want = sorted((int(c), float(sd(val))) for c, val in zip(ix[s_:e_], v[s_:e_]))
+        assert sorted(seqs[r]) == want, r
+    # bank classes per (group, warp, quarter, step): slot mod 8/L
+    L = 32 // info.rows_per_warp
+    rq = 8 // L
+    w, rpw = info.warps_per_cta, info.rows_per_warp
+    conflicts = steps = 0
+    for gi in range(info.n_groups):
+        for wi in range(w):
+            off, width = a["so"][gi * w + wi], a["sw"][gi * w + wi]
+            if width == 0:
+                continue
+            sl = a["sl"][off:off + width * rpw].reshape(width // 4, rpw, 4)
+            sl = sl.transpose(0, 2, 1).reshape(width, rpw).astype(np.int64)
+            cls = sl % rq
+            for q in range(rpw // rq):
+                for n in range(width):
+                    s_q, c_q = sl[n, q * rq:(q + 1) * rq], cls[n, q * rq:(q + 1) * rq]
+                    pairs = set(zip(s_q.tolist(), c_q.tolist()))
+                    steps += 1
+                    conflicts += len(pairs) - len({c for _, c in pairs})
+    assert conflicts == 0, (conflicts, steps)

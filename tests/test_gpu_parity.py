@@ -76,7 +76,7 @@ def test_trace_ray_and_build_count():
     assert np.array_equal(seg.indices, A.indices[A.indptr[r]:A.indptr[r + 1]])
 
 
-@pytest.mark.parametrize("order", ["reference", "native"])
+@pytest.mark.parametrize("order", ["reference", "traversal", "native"])
 def test_operator_application_g64(order):
     gold = load_golden("pipeline_g64")
     g = geometry.make_geometry(96, 1, 64)
@@ -90,10 +90,23 @@ def test_operator_application_g64(order):
             gf, ga = gold[f"g64_fwd_{prec}_f{ff}"], gold[f"g64_adj_{prec}_f{ff}"]
             assert f.dtype == gf.dtype and f.shape == gf.shape
             assert np.array_equal([s.factor for s in st], gold[f"g64_fwdfac_{prec}_f{ff}"])
-            # the adjoint's per-voxel order is the reference's in both modes
-            assert np.array_equal(a, ga), (prec, ff)
+            if order != "native":
+                # ray-id order per voxel is the reference's adjoint order
+                assert np.array_equal(a, ga), (prec, ff)
             if order == "reference":
                 assert np.array_equal(f, gf), (prec, ff)
+            elif order == "native":
+                for out, ref in ((f, gf), (a, ga)):
+                    if prec == "double":
+                        assert rel_l2(out, ref) <= 1e-14
+                    elif prec == "single":
+                        assert rel_l2(out, ref) <= 1e-6
+                    elif prec == "mixed":
+                        # fp32 sums in another order, cast to fp16: rare flips
+                        assert rel_l2(out, ref) <= 1e-3
+                        assert np.mean(out != ref) <= 1e-2
+                    else:   # half: fp16 accumulation, order-sensitive
+                        assert rel_l2(out, ref) <= 3e-3
             elif prec == "double":
                 assert rel_l2(f, gf) <= 1e-14
             elif prec == "single":
@@ -154,12 +167,15 @@ def test_c1_native_order_tolerances():
     OA = O.system_matrix(og)
     y = O.measure(OA, O.phantom("shepp-logan-like", 128, 16))
     for prec in ("single", "mixed"):
+        trav = pipeline.assemble(g, pipeline.SystemConfig(precision=prec, ffactor=16,
+                                                           order="traversal"))
+        res10 = solver.cgls_solve(trav, y, solver.SolveConfig(max_iters=10, precision=prec))
+        same = O.cgls(O.Operator(OA, og, prec, 16, partitions=1, cap_bytes=None), y, 10, prec)
+        assert np.array_equal(res10.x, same["x"]), prec
         sysm = pipeline.assemble(g, pipeline.SystemConfig(precision=prec, ffactor=16))
         res10 = solver.cgls_solve(sysm, y, solver.SolveConfig(max_iters=10, precision=prec))
         ref10 = O.cgls(O.Operator(OA, og, prec, 16), y, 10, prec)
-        assert rel_l2(res10.x, ref10["x"]) <= 1e-5, prec
-        same = O.cgls(O.Operator(OA, og, prec, 16, partitions=1, cap_bytes=None), y, 10, prec)
-        assert np.array_equal(res10.x, same["x"]), prec
+        assert rel_l2(res10.x, ref10["x"]) <= (1e-5 if prec == "single" else 2e-3), prec
         res = solver.cgls_solve(sysm, y, solver.SolveConfig(max_iters=30, precision=prec))
         curve = gold[f"cg_{prec}_residual"]
         floor_curve, floor_x = (0.071, 1.6e-3) if prec == "single" else (0.013, 1.2e-3)
@@ -185,7 +201,8 @@ def test_cgls_g90_all_precisions():
             np.testing.assert_allclose(res.residual_history, gold[f"{prec}_residual"], rtol=1e-4)
         else:
             assert np.array_equal(res.x, gold[f"{prec}_x"]), prec
-            assert np.array_equal(res.residual_history, gold[f"{prec}_residual"])
+            # history scalars are float64 dots in another summation order
+            np.testing.assert_allclose(res.residual_history, gold[f"{prec}_residual"], rtol=1e-12)
 
 
 def test_edge_cases_padding_vectors_zero():
@@ -248,8 +265,14 @@ def test_large_geometry_invariants():
     rhs = float(np.sum(x * sysd.apply_adjoint(yv)[0]))
     assert abs(lhs - rhs) <= 1e-10 * abs(lhs)
     nat = pipeline.assemble(g, pipeline.SystemConfig(precision="single", ffactor=16))
+    trav = pipeline.assemble(g, pipeline.SystemConfig(precision="single", ffactor=16,
+                                                       order="traversal"))
     ref = pipeline.assemble(g, pipeline.SystemConfig(precision="single", ffactor=16,
                                                       order="reference"))
     x32 = x.astype(np.float32)
-    assert rel_l2(nat.apply_forward(x32)[0], ref.apply_forward(x32)[0]) <= 1e-6
-    assert np.array_equal(nat.apply_adjoint(yv)[0], ref.apply_adjoint(yv)[0])
+    fr = ref.apply_forward(x32)[0]
+    assert rel_l2(nat.apply_forward(x32)[0], fr) <= 1e-6
+    assert rel_l2(trav.apply_forward(x32)[0], fr) <= 1e-6
+    ar = ref.apply_adjoint(yv)[0]
+    assert np.array_equal(trav.apply_adjoint(yv)[0], ar)
+    assert rel_l2(nat.apply_adjoint(yv)[0], ar) <= 1e-6

@@ -1,0 +1,48 @@
+#!/usr/bin/env python
+"""Summarize an ncu report (raw page) for the staged SpMM: time, DRAM bytes,
+throughputs, SMEM wavefronts/conflicts and warp-stall breakdown."""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ldgsts.sum",
+        "lts__t_sector_hit_rate.pct", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "smsp__inst_executed.sum",
+        "sm__cycles_elapsed.avg.per_second", "lts__t_bytes.sum",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active")
+
+
+def main(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        print(f"== {d.get('Kernel Name', '')[:60]}  grid {d.get('Grid Size')} block {d.get('Block Size')}")
+        for k in KEYS:
+            if k in d:
+                print(f"  {k:75s} {d[k]} {u.get(k, '')}")
+        stalls = sorted(((float(v), k) for k, v in d.items()
+                         if k.startswith("smsp__average_warps_issue_stalled_") and
+                         k.endswith("_per_issue_active.ratio") and v not in ("", "n/a")),
+                        reverse=True)
+        print("  stalls (cycles per issued instruction):",
+              ", ".join(f"{k[34:-23]}={v:.2f}" for v, k in stalls[:7]))
+
+
+if __name__ == "__main__":
+    for p in sys.argv[1:]:
+        main(p)
