@@ -227,18 +227,30 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     from paper_2009_07226_b200 import _lib, geometry, pipeline, solver
 
+    from paper_2009_07226_b200 import parallel
+    scfg = pipeline.SystemConfig(precision=cfg["precision"], ffactor=16, order=args.order)
     t0 = time.perf_counter()
-    g, A, y = make_problem(cfg, cfg["slices"], dev)
-    nnz = A.nnz
-    t_matrix = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    system = pipeline.assemble(g, pipeline.SystemConfig(precision=cfg["precision"], ffactor=16,
-                                                         order=args.order))
+    system, t_matrix = None, 0.0
+    if rank == 0:
+        g, A, y = make_problem(cfg, cfg["slices"], dev)
+        t_matrix = time.perf_counter() - t0
+        system = pipeline.assemble(g, scfg)
+        geometry.clear_matrix_cache()
+        A.d_indices = A.d_values = None      # keep HBM for the run
+        torch.cuda.empty_cache()
+    else:
+        g = geometry.make_geometry(cfg["k"], cfg["slices"], cfg["n"])
+    if ws > 1:
+        # one host build; the staged operator goes to every GPU over NVLink
+        system = parallel.broadcast_system(system, scfg, g)
+        y1 = [y[:, :1].contiguous() if rank == 0 else None]
+        yt = y1[0] if rank == 0 else torch.empty((g.num_rays, 1), dtype=torch.float64,
+                                                  device=dev)
+        dist.broadcast(yt, src=0)
+        y = yt.repeat(1, cfg["slices"]).contiguous()
     torch.cuda.synchronize()
-    t_assemble = time.perf_counter() - t0
-    geometry.clear_matrix_cache()
-    A.d_indices = A.d_values = None          # keep HBM for the run
-    torch.cuda.empty_cache()
+    t_assemble = time.perf_counter() - t0 - t_matrix
+    nnz = system.matrix.nnz
 
     S = cfg["slices"]
     W, K = max(args.warmup, 0), max(args.steps, 1)

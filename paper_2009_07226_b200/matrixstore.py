@@ -409,6 +409,15 @@ def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndar
     t["cta_rows"] = torch.from_numpy(rows.reshape(-1)).to(dev)
     side = DeviceSide(precision, ffactor, f_dev, n_cols, n_rows, value_scale_exp, info, t,
                       plan_kind=plan.kind)
+    return attach(side)
+
+
+INFO_FIELDS = [f for f, _ in _lib.FormatInfo._fields_]
+
+
+def attach(side: DeviceSide) -> DeviceSide:
+    """(Re)bind the kernel descriptor of a side to its device tensors."""
+    info, t = side.info, side.tensors
     s = _lib.Staged()
     s.n_cta, s.rows_per_cta = info.n_cta, info.rows_per_cta
     s.warps_per_cta, s.rows_per_warp = info.warps_per_cta, info.rows_per_warp
@@ -422,5 +431,27 @@ def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndar
     s.d_slots = t["slots"].data_ptr()
     s.d_values = t["values"].data_ptr()
     side.staged = s
+    plane_slots = -(-int(info.max_group_slots) // 8) * 8
+    rec = side.f_dev * element_bytes(side.precision)
     side.smem_bytes = int(2 * (plane_slots * rec + 128))
     return side
+
+
+def side_meta(side: DeviceSide) -> dict:
+    """Picklable description of a side (everything but the tensor data)."""
+    return dict(precision=side.precision, ffactor=side.ffactor, f_dev=side.f_dev,
+                n_in=side.n_in, n_out=side.n_out, value_scale_exp=side.value_scale_exp,
+                plan_kind=side.plan_kind,
+                info={f: getattr(side.info, f) for f in INFO_FIELDS},
+                tensors={k: (tuple(v.shape), str(v.dtype).replace("torch.", ""))
+                         for k, v in side.tensors.items()})
+
+
+def side_from_meta(meta: dict, tensors: dict) -> DeviceSide:
+    info = _lib.FormatInfo()
+    for f, v in meta["info"].items():
+        setattr(info, f, v)
+    side = DeviceSide(meta["precision"], meta["ffactor"], meta["f_dev"], meta["n_in"],
+                      meta["n_out"], meta["value_scale_exp"], info, tensors,
+                      plan_kind=meta["plan_kind"])
+    return attach(side)

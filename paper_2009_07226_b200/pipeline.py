@@ -141,6 +141,19 @@ class AssembledSystem:
                 raise ValueError("data parallelism beyond P_d=1 needs a scan geometry")
             self._build_partitioned(ip, ix, v, n_rows, n_cols)
 
+    @classmethod
+    def from_sides(cls, matrix, config: SystemConfig, geometry, forward_block, adjoint_block,
+                   value_scale_exp: int) -> "AssembledSystem":
+        """Wrap already-built device sides (e.g. received by broadcast)."""
+        self = cls.__new__(cls)
+        self.matrix, self.config, self.geometry = matrix, config, geometry
+        self.device = device()
+        self.value_scale_exp = value_scale_exp
+        n_rows, n_cols = int(matrix.num_rows), int(matrix.num_cols)
+        self.forward = _Side([forward_block], [None], [None], [np.arange(n_rows)], n_cols, n_rows)
+        self.adjoint = _Side([adjoint_block], [None], [None], [np.arange(n_cols)], n_rows, n_cols)
+        return self
+
     # -- construction ---------------------------------------------------------
 
     def _plan(self, ip, ix, n_rows, n_cols, kind):
