@@ -236,7 +236,7 @@ def main():
         t_matrix = time.perf_counter() - t0
         system = pipeline.assemble(g, scfg)
         geometry.clear_matrix_cache()
-        A.d_indices = A.d_values = None      # keep HBM for the run
+        A.release_device()                   # keep HBM for the run
         torch.cuda.empty_cache()
     else:
         g = geometry.make_geometry(cfg["k"], cfg["slices"], cfg["n"])

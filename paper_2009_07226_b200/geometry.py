@@ -157,7 +157,12 @@ class SystemMatrix:
         self.num_rows, self.num_cols = num_rows, num_cols
         self.num_angles, self.num_detector_cols = num_angles, num_detector_cols
         self.d_indptr, self.d_indices, self.d_values = d_indptr, d_indices, d_values
+        self._nnz = int(d_indices.numel())
         self._host = None
+
+    def release_device(self) -> None:
+        """Drop the device CSR (keeps host copies if already materialized)."""
+        self.d_indptr = self.d_indices = self.d_values = None
 
     @classmethod
     def from_host(cls, num_rows, num_cols, indptr, indices, values, num_angles=None,
@@ -193,7 +198,7 @@ class SystemMatrix:
 
     @property
     def nnz(self) -> int:
-        return int(self.d_indices.numel())
+        return self._nnz
 
     def host_csr32(self):
         """(indptr i64, indices i32, values f64) host arrays for the builders."""
