@@ -59,6 +59,16 @@ int xct_siddon_fill(const double* d_cos, const double* d_sin, int k0, int k1,
                     const int64_t* d_rowptr /* [(k1-k0)*n_det+1], relative */,
                     int32_t* d_indices, double* d_values, void* stream);
 
+/* Column-range restriction of a device CSR for the streamed operator build
+ * (the back-projection format is built one band of voxels at a time; cf.
+ * matrixstore._restrict_rows, src/matrixstore.py:151-165).  Count pass when
+ * d_counts != NULL (entries per row with col in [col_lo, col_hi)), else fill
+ * pass into d_out_ptr/d_out_idx (col - col_lo)/d_out_val, order preserved. */
+int xct_csr_filter_cols(const int64_t* d_indptr, const int32_t* d_indices,
+                        const double* d_values, int64_t n_rows, int32_t col_lo,
+                        int32_t col_hi, int64_t* d_counts, const int64_t* d_out_ptr,
+                        int32_t* d_out_idx, double* d_out_val, void* stream);
+
 /* ---------------------------------------------------------------------------
  * K5  staged execution format (host builder)
  * replaces matrixstore.build_staged / pack (src/matrixstore.py:250-262,

@@ -181,3 +181,60 @@ extern "C" int xct_siddon_fill(const double* d_cos, const double* d_sin, int k0,
   XCT_CUDA_CHECK_LAUNCH("siddon_fill");
   return XCT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Column-range restriction of a device CSR (streamed operator build: the
+// back-projection format is built per band of voxels, src/matrixstore.py:
+// 151-165 restricts rows the same way).  Count pass, then fill with columns
+// rebased to col_lo; rows keep their order and their entries' CSR order.
+namespace {
+__global__ void csr_filter_count_kernel(const int64_t* __restrict__ indptr,
+                                        const int32_t* __restrict__ indices, int64_t n_rows,
+                                        int32_t lo, int32_t hi, int64_t* __restrict__ counts) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = 0;
+    for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) c += (indices[j] >= lo && indices[j] < hi);
+    counts[r] = c;
+  }
+}
+__global__ void csr_filter_fill_kernel(const int64_t* __restrict__ indptr,
+                                       const int32_t* __restrict__ indices,
+                                       const double* __restrict__ values, int64_t n_rows,
+                                       int32_t lo, int32_t hi, const int64_t* __restrict__ out_ptr,
+                                       int32_t* __restrict__ out_idx, double* __restrict__ out_val) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = out_ptr[r];
+    for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) {
+      const int32_t c = indices[j];
+      if (c >= lo && c < hi) {
+        out_idx[o] = c - lo;
+        out_val[o] = values[j];
+        ++o;
+      }
+    }
+  }
+}
+}  // namespace
+
+extern "C" int xct_csr_filter_cols(const int64_t* d_indptr, const int32_t* d_indices,
+                                   const double* d_values, int64_t n_rows, int32_t col_lo,
+                                   int32_t col_hi, int64_t* d_counts, const int64_t* d_out_ptr,
+                                   int32_t* d_out_idx, double* d_out_val, void* stream) {
+  if (!d_indptr || n_rows < 0 || col_hi < col_lo)
+    return xct::fail(XCT_EINVAL, "csr_filter_cols: bad argument");
+  if (n_rows == 0) return XCT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d_counts) {
+    csr_filter_count_kernel<<<grid_for(n_rows, 128), 128, 0, s>>>(d_indptr, d_indices, n_rows,
+                                                                 col_lo, col_hi, d_counts);
+  } else {
+    if (!d_out_ptr || !d_out_idx || !d_out_val)
+      return xct::fail(XCT_EINVAL, "csr_filter_cols: fill pass needs output arrays");
+    csr_filter_fill_kernel<<<grid_for(n_rows, 128), 128, 0, s>>>(
+        d_indptr, d_indices, d_values, n_rows, col_lo, col_hi, d_out_ptr, d_out_idx, d_out_val);
+  }
+  XCT_CUDA_CHECK_LAUNCH("csr_filter_cols");
+  return XCT_OK;
+}

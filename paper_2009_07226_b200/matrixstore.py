@@ -52,6 +52,7 @@ _STORE = {"double": np.float64, "single": np.float32, "half": np.float16, "mixed
 _COMPUTE = {"double": np.float64, "single": np.float32, "half": np.float16, "mixed": np.float32}
 
 StageSplitRequired = _lib.StageSplitError
+INFO_FIELDS = [f for f, _ in _lib.FormatInfo._fields_]
 
 
 def _check_precision(precision: str) -> None:
@@ -189,29 +190,36 @@ def _roundup(a, b):
     return -(-a // b) * b
 
 
-def forward_plan(num_angles: int, n: int, rows_per_warp: int, warps: int) -> Plan:
+def forward_plan(num_angles: int, n: int, rows_per_warp: int, warps: int,
+                 k0: int = 0, k1: int | None = None) -> Plan:
     """Projection A (rows = rays k*N + c): CTA tiles of `ta` views x `td`
     detectors, one warp = rows_per_warp consecutive detectors of one view.
     Load groups are image bands across the dominant ray direction: z bands
     for steep views, x bands (ascending for cos>0, descending for cos<0) for
-    shallow ones, so a ray's entries stay in traversal order."""
+    shallow ones, so a ray's entries stay in traversal order.
+    [k0, k1) restricts the tiles to a range of views (k0 a multiple of the
+    tile height); row ids stay global."""
     rw = rows_per_warp
     td = min(_roundup(n, rw), max(rw, 32))
     rpc = max(td, (rw * warps) // td * td)
     ta = rpc // td
-    n_ta, n_td = -(-num_angles // ta), -(-n // td)
+    k1 = num_angles if k1 is None else k1
+    n_ta, n_td = -(-(k1 - k0) // ta), -(-n // td)
     cells = pseudo_hilbert_cells(n_td, n_ta)           # (x = det tile, z = view tile)
     ai, di = np.divmod(np.arange(rpc), td)
-    k = cells[:, 1:2] * ta + ai[None, :]
+    k = k0 + cells[:, 1:2] * ta + ai[None, :]
     c = cells[:, 0:1] * td + di[None, :]
-    rows = np.where((k < num_angles) & (c < n), k * n + c, -1).astype(np.int32)
-    # regime per tile from its views' directions
-    step = math.pi / max(num_angles, 1)
-    del step
+    rows = np.where((k < k1) & (c < n), k * n + c, -1).astype(np.int32)
     cols = np.arange(n * n, dtype=np.int64)
     iz, ix = np.divmod(cols, n)
     tables = np.stack([iz, ix, n - 1 - ix]).astype(np.int32)
     return Plan(rows, tables, np.zeros(len(rows), np.int32), rw, "forward")
+
+
+def forward_tile_height(n: int, rows_per_warp: int, warps: int) -> int:
+    rw = rows_per_warp
+    td = min(_roundup(n, rw), max(rw, 32))
+    return max(td, (rw * warps) // td * td) // td
 
 
 def assign_forward_regimes(plan: Plan, angles, n: int) -> Plan:
@@ -234,22 +242,31 @@ def assign_forward_regimes(plan: Plan, angles, n: int) -> Plan:
     return plan
 
 
-def adjoint_plan(num_angles: int, n: int, rows_per_warp: int, warps: int) -> Plan:
+def adjoint_plan(num_angles: int, n: int, rows_per_warp: int, warps: int,
+                 z0: int = 0, z1: int | None = None) -> Plan:
     """Back projection A^T (rows = voxels iz*N + ix): CTA tiles of tz x tx
     voxels, a warp = rows_per_warp consecutive voxels of one image row.
-    Load groups are ranges of view angles (key = ray // N)."""
+    Load groups are ranges of view angles (key = ray // N).  [z0, z1)
+    restricts the tiles to a band of image rows (z0 a multiple of tz)."""
     rw = rows_per_warp
     tx = min(_roundup(n, rw), max(rw, 16))
     rpc = max(tx, (rw * warps) // tx * tx)
     tz = rpc // tx
-    n_tz, n_tx = -(-n // tz), -(-n // tx)
+    z1 = n if z1 is None else z1
+    n_tz, n_tx = -(-(z1 - z0) // tz), -(-n // tx)
     cells = pseudo_hilbert_cells(n_tx, n_tz)
     zi, xi = np.divmod(np.arange(rpc), tx)
-    z = cells[:, 1:2] * tz + zi[None, :]
+    z = z0 + cells[:, 1:2] * tz + zi[None, :]
     x = cells[:, 0:1] * tx + xi[None, :]
-    rows = np.where((z < n) & (x < n), z * n + x, -1).astype(np.int32)
+    rows = np.where((z < z1) & (x < n), z * n + x, -1).astype(np.int32)
     tables = (np.arange(num_angles * n, dtype=np.int64) // n).astype(np.int32)[None, :]
     return Plan(rows, tables, np.zeros(len(rows), np.int32), rw, "adjoint")
+
+
+def adjoint_tile_height(n: int, rows_per_warp: int, warps: int) -> int:
+    rw = rows_per_warp
+    tx = min(_roundup(n, rw), max(rw, 16))
+    return max(tx, (rw * warps) // tx * tx) // tx
 
 
 def row_block_plan(n_rows: int, n_cols: int, rows_per_warp: int, warps: int,
@@ -344,15 +361,22 @@ class DeviceSide:
         return sum(int(t.numel() * t.element_size()) for t in self.tensors.values())
 
 
-def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndarray,
-                      n_rows: int, n_cols: int, plan: Plan, precision: str, ffactor: int,
-                      value_scale_exp: int, smem_budget: int = SMEM_BUDGET,
-                      dev=None, schedule: bool = False) -> DeviceSide:
-    """Build the staged format on the host (libxct_b200 K5) and upload it."""
-    import torch
-    from .geometry import device
+@dataclass
+class HostFormat:
+    """Exported K5 format on the host (exact-size arrays) plus its rows."""
+
+    arrays: dict
+    info: dict
+    cta_rows: np.ndarray
+    plan_kind: str
+
+
+def build_format(indptr: np.ndarray, indices32: np.ndarray, values: np.ndarray,
+                 n_rows: int, n_cols: int, plan: Plan, precision: str, ffactor: int,
+                 value_scale_exp: int, smem_budget: int = SMEM_BUDGET,
+                 schedule: bool = False) -> HostFormat:
+    """Run the K5 host builder (libxct_b200) and export its arrays."""
     _check_precision(precision)
-    dev = dev or device()
     f_dev = f_dev_for(ffactor, precision)
     rec = f_dev * element_bytes(precision)
     # the kernel double-buffers the stage: two groups of `capacity` records
@@ -367,7 +391,8 @@ def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndar
     L = _lib.lib()
     lp = (rec // 16).bit_length() - 1
     lg = (32 // plan.rows_per_warp).bit_length() - 1
-    st = L.xct_format_build(n_rows, n_cols, ip.ctypes.data, ix.ctypes.data, vals.ctypes.data,
+    st = L.xct_format_build(n_rows, n_cols, ip.ctypes.data, ix.ctypes.data if len(ix) else None,
+                            vals.ctypes.data if len(vals) else None,
                             rows.shape[0], rows.shape[1], plan.rows_per_warp,
                             rows.ctypes.data, keys.ctypes.data, ctab.ctypes.data, capacity,
                             _lib.PREC_CODE[precision], int(value_scale_exp),
@@ -378,41 +403,104 @@ def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndar
         info = _lib.FormatInfo()
         _lib.check(L.xct_format_get_info(handle, C.byref(info)), "xct_format_get_info")
         warps = int(info.warps_per_cta)
-        h = dict(cta_group_ptr=np.empty(info.n_cta + 1, np.int32),
-                 group_map_ptr=np.empty(info.n_groups + 1, np.int64),
-                 group_map=np.empty(max(info.n_slots, 1), np.int32),
-                 slab_off=np.empty(max(info.n_groups * warps, 1), np.int64),
-                 slab_width=np.empty(max(info.n_groups * warps, 1), np.int32),
-                 slots=np.empty(max(info.n_padded, 1), np.uint16),
-                 values=np.empty(max(info.n_padded, 1), storage_dtype(precision)))
+        sizes = dict(cta_group_ptr=info.n_cta + 1, group_map_ptr=info.n_groups + 1,
+                     group_map=info.n_slots, slab_off=info.n_groups * warps,
+                     slab_width=info.n_groups * warps, slots=info.n_padded,
+                     values=info.n_padded)
+        dts = dict(cta_group_ptr=np.int32, group_map_ptr=np.int64, group_map=np.int32,
+                   slab_off=np.int64, slab_width=np.int32, slots=np.uint16,
+                   values=storage_dtype(precision))
+        h = {k: np.empty(max(int(n), 1), dts[k]) for k, n in sizes.items()}
         _lib.check(L.xct_format_export(handle, *[h[k].ctypes.data for k in
                                                  ("cta_group_ptr", "group_map_ptr", "group_map",
                                                   "slab_off", "slab_width", "slots", "values")]),
                    "xct_format_export")
     finally:
         L.xct_format_free(handle)
+    h = {k: v[:int(sizes[k])] for k, v in h.items()}
+    return HostFormat(h, {f: getattr(info, f) for f in INFO_FIELDS}, rows.reshape(-1),
+                      plan.kind)
+
+
+def concat_formats(parts: list) -> HostFormat:
+    """Concatenate formats of disjoint CTA-tile sets built separately (e.g.
+    streamed over angle or voxel chunks): offsets are rebased."""
+    if len(parts) == 1:
+        return parts[0]
+    i0 = parts[0].info
+    out = {k: [] for k in parts[0].arrays}
+    rows = []
+    g_off = s_off = e_off = 0
+    for hf in parts:
+        a, inf = hf.arrays, hf.info
+        for k in ("rows_per_cta", "rows_per_warp", "warps_per_cta", "value_bytes"):
+            if inf[k] != i0[k]:
+                raise ValueError(f"cannot concatenate formats with different {k}")
+        out["cta_group_ptr"].append(a["cta_group_ptr"][:-1] + g_off)
+        out["group_map_ptr"].append(a["group_map_ptr"][:-1] + s_off)
+        out["group_map"].append(a["group_map"])
+        out["slab_off"].append(a["slab_off"] + e_off)
+        out["slab_width"].append(a["slab_width"])
+        out["slots"].append(a["slots"])
+        out["values"].append(a["values"])
+        rows.append(hf.cta_rows)
+        g_off += int(inf["n_groups"])
+        s_off += int(inf["n_slots"])
+        e_off += int(inf["n_padded"])
+    out["cta_group_ptr"].append(np.array([g_off], np.int32))
+    out["group_map_ptr"].append(np.array([s_off], np.int64))
+    arrays = {k: np.concatenate(v) for k, v in out.items()}
+    info = dict(i0)
+    for k in ("n_cta", "n_groups", "n_slots", "n_padded", "nnz", "underflow_count"):
+        info[k] = sum(int(hf.info[k]) for hf in parts)
+    info["max_group_slots"] = max(int(hf.info["max_group_slots"]) for hf in parts)
+    info["max_rel_quant_error"] = max(float(hf.info["max_rel_quant_error"]) for hf in parts)
+    return HostFormat(arrays, info, np.concatenate(rows), parts[0].plan_kind)
+
+
+def upload_format(hf: HostFormat, precision: str, ffactor: int, n_in: int, n_out: int,
+                  value_scale_exp: int, dev=None) -> "DeviceSide":
+    """Encode the entries for K6 and move the format to HBM."""
+    import torch
+    from .geometry import device
+    dev = dev or device()
+    h = dict(hf.arrays)
+    f_dev = f_dev_for(ffactor, precision)
     # K6 addresses a staged record by its byte offset inside a plane
-    plane_slots = -(-int(info.max_group_slots) // 8) * 8
+    plane_slots = -(-int(hf.info["max_group_slots"]) // 8) * 8
     if plane_slots * 16 > 65536:
         raise StageSplitRequired("load group too large for 16-bit plane offsets")
     h["slots"] = (h["slots"].astype(np.uint32) << 4).astype(np.uint16)
     if precision in ("half", "mixed"):
         # one 32-bit word per entry: byte offset << 16 | fp16 length
-        h["values"] = (h["slots"].astype(np.uint32) << 16) | h["values"].view(np.uint16)
-        h["values"] = h["values"].view(np.int32)
+        h["values"] = ((h["slots"].astype(np.uint32) << 16) |
+                       h["values"].view(np.uint16)).view(np.int32)
         h["slots"] = np.zeros(1, np.uint16)
     # the kernel's load ring reads up to 4 steps (x 32 rows x 4) past a slab
     for k in ("slots", "values"):
         h[k] = np.concatenate([h[k], np.zeros(1024, h[k].dtype)])
+    for k in ("group_map", "slab_off", "slab_width"):
+        if len(h[k]) == 0:
+            h[k] = np.zeros(1, h[k].dtype)
     t = {k: torch.from_numpy(v.view(np.int16) if v.dtype == np.uint16 else v).to(dev)
          for k, v in h.items()}
-    t["cta_rows"] = torch.from_numpy(rows.reshape(-1)).to(dev)
-    side = DeviceSide(precision, ffactor, f_dev, n_cols, n_rows, value_scale_exp, info, t,
-                      plan_kind=plan.kind)
+    t["cta_rows"] = torch.from_numpy(np.ascontiguousarray(hf.cta_rows, np.int32)).to(dev)
+    info = _lib.FormatInfo()
+    for f, v in hf.info.items():
+        setattr(info, f, v)
+    side = DeviceSide(precision, ffactor, f_dev, n_in, n_out, value_scale_exp, info, t,
+                      plan_kind=hf.plan_kind)
     return attach(side)
 
 
-INFO_FIELDS = [f for f, _ in _lib.FormatInfo._fields_]
+def build_device_side(indptr: np.ndarray, indices32: np.ndarray, values: np.ndarray,
+                      n_rows: int, n_cols: int, plan: Plan, precision: str, ffactor: int,
+                      value_scale_exp: int, smem_budget: int = SMEM_BUDGET,
+                      dev=None, schedule: bool = False) -> "DeviceSide":
+    """Build the staged format on the host (libxct_b200 K5) and upload it."""
+    hf = build_format(indptr, indices32, values, n_rows, n_cols, plan, precision, ffactor,
+                      value_scale_exp, smem_budget, schedule)
+    return upload_format(hf, precision, ffactor, n_cols, n_rows, value_scale_exp, dev)
 
 
 def attach(side: DeviceSide) -> DeviceSide:

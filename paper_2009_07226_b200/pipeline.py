@@ -49,6 +49,10 @@ class SystemConfig:
                      to the reference's default configuration.
       warps_per_cta  CTA size of the staged SpMM.
       smem_budget    shared-memory bytes per CTA for one load group.
+      build          "streamed": never materialize the whole matrix -- the
+                     projection format is built per chunk of views, the back
+                     projection per band of voxels, from Siddon regenerated
+                     on the device ("auto": streamed above STREAM_NNZ).
     ``topology`` and ``comm_strategy`` are accepted for API compatibility;
     on one NVSwitch box the exchange has a single level.
     """
@@ -66,6 +70,7 @@ class SystemConfig:
     order: str = "native"
     warps_per_cta: int = 16
     smem_budget: int = matrixstore.SMEM_BUDGET
+    build: str = "auto"
 
     def __post_init__(self):
         if self.precision not in matrixstore.PRECISIONS:
@@ -78,6 +83,8 @@ class SystemConfig:
             raise ValueError(f"unknown order {self.order!r}; expected one of {ORDERS}")
         if self.p_b < 1 or self.p_d < 1:
             raise ValueError("P_b and P_d must be >= 1")
+        if self.build not in ("auto", "monolithic", "streamed"):
+            raise ValueError(f"unknown build mode {self.build!r}")
 
 
 @dataclass
@@ -360,8 +367,21 @@ class AssembledSystem:
         return sum(b.hbm_bytes() for s in (self.forward, self.adjoint) for b in s.blocks)
 
 
+STREAM_NNZ = 6e8        # auto mode streams operators larger than this
+
+
+def _streamable(geometry, config) -> bool:
+    if config.p_d != 1 or config.order == "reference" or config.build == "monolithic":
+        return False
+    if config.build == "streamed":
+        return True
+    return 1.2 * geometry.num_angles * geometry.grid_n ** 2 > STREAM_NNZ
+
+
 def assemble(geometry: ScanGeometry, config: SystemConfig) -> AssembledSystem:
     """Build the device operator for a scan geometry (matrix memoized)."""
+    if _streamable(geometry, config):
+        return StreamedAssembly(geometry, config).run()
     return AssembledSystem(build_system_matrix(geometry), config, geometry=geometry)
 
 
@@ -371,3 +391,147 @@ def assemble_from_matrix(matrix, config: SystemConfig | None = None) -> Assemble
     if config.p_d != 1:
         config = replace(config, p_d=1)
     return AssembledSystem(matrix, config, geometry=None)
+
+
+class StreamedAssembly:
+    """Operator build that never holds the whole matrix (needed at 2048^2 x
+    2048 views, 1.03e10 entries): Siddon is regenerated on the device per
+    chunk of views; the projection format is built chunk by chunk, the back
+    projection format band of voxel rows by band (each band's entries are
+    the column-restricted chunks, transposed on the host).  Per-row orders
+    and load groups are exactly those of the monolithic build."""
+
+    CHUNK_NNZ = 4e8          # entries per Siddon chunk on the device / host
+    BAND_NNZ = 1.2e9         # entries per back-projection band on the host
+
+    def __init__(self, geometry: ScanGeometry, config: SystemConfig):
+        self.g, self.cfg = geometry, config
+        self.dev = device()
+        self.rw = _rows_per_warp(config)
+
+    def _chunks(self, align: int):
+        g = self.g
+        per = max(1, int(self.CHUNK_NNZ // (1.2 * g.grid_n ** 2)))
+        per = max(align, per // align * align)
+        return [(k, min(k + per, g.num_angles)) for k in range(0, g.num_angles, per)]
+
+    def _siddon(self, k0, k1):
+        from .geometry import siddon_csr
+        return siddon_csr(self.g, k0, k1, self.dev)
+
+    def _exponent(self, chunks) -> int:
+        """half_rescale_exponent over the whole matrix without holding it:
+        exact binade histogram of the positive lengths, then the two middle
+        values when they straddle a binade (numpy median: their mean)."""
+        import torch
+        hist = torch.zeros(2048, dtype=torch.int64, device=self.dev)
+        for k0, k1 in chunks:
+            _, _, v = self._siddon(k0, k1)
+            pos = v[v > 0]
+            hist += torch.bincount((pos.view(torch.int64) >> 52), minlength=2048)
+        n = int(hist.sum())
+        if n == 0:
+            return 0
+        cum = torch.cumsum(hist, 0).cpu().numpy()
+        lo_rank, hi_rank = (n - 1) // 2, n // 2                 # 0-based middle ranks
+        b_lo = int(np.searchsorted(cum, lo_rank, side="right"))
+        b_hi = int(np.searchsorted(cum, hi_rank, side="right"))
+        if b_lo == b_hi:
+            return -(b_lo - 1023)
+        # two middle values in adjacent binades: largest of b_lo, smallest of b_hi
+        big, small = -math.inf, math.inf
+        for k0, k1 in chunks:
+            _, _, v = self._siddon(k0, k1)
+            e = (v.view(torch.int64) >> 52)
+            a = v[(v > 0) & (e == b_lo)]
+            b = v[(v > 0) & (e == b_hi)]
+            if a.numel():
+                big = max(big, float(a.max()))
+            if b.numel():
+                small = min(small, float(b.min()))
+        return -int(math.floor(math.log2((big + small) / 2.0)))
+
+    def _forward(self, exp):
+        cfg, g = self.cfg, self.g
+        n = g.grid_n
+        ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta)
+        parts = []
+        for k0, k1 in self._chunks(ta):
+            plan = matrixstore.forward_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, k0, k1)
+            plan = matrixstore.assign_forward_regimes(plan, g.angles, n)
+            base = k0 * n
+            plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - base, -1).astype(np.int32)
+            ip, ix, v = self._siddon(k0, k1)
+            ip, ix, v = ip.cpu().numpy(), ix.cpu().numpy(), v.cpu().numpy()
+            hf = matrixstore.build_format(ip, ix, v, (k1 - k0) * n, g.num_voxels, plan,
+                                          cfg.precision, cfg.ffactor, exp, cfg.smem_budget,
+                                          schedule=cfg.order == "native")
+            hf.cta_rows = np.where(hf.cta_rows >= 0, hf.cta_rows + base, -1).astype(np.int32)
+            parts.append(hf)
+            self.nnz += int(hf.info["nnz"])
+        hf = matrixstore.concat_formats(parts)
+        del parts
+        return matrixstore.upload_format(hf, cfg.precision, cfg.ffactor, g.num_voxels,
+                                         g.num_rays, exp, self.dev)
+
+    def _adjoint(self, exp, chunks):
+        import torch
+        cfg, g = self.cfg, self.g
+        n, R = g.grid_n, g.num_rays
+        tz = matrixstore.adjoint_tile_height(n, self.rw, cfg.warps_per_cta)
+        per = max(1, int(self.BAND_NNZ // (1.2 * g.num_angles * n)))
+        per = max(tz, per // tz * tz)
+        st = _lib.stream_handle(self.dev)
+        parts = []
+        for z0 in range(0, n, per):
+            z1 = min(n, z0 + per)
+            lo, hi = z0 * n, z1 * n
+            counts, idx, val = [], [], []
+            for k0, k1 in chunks:
+                ip, ix, v = self._siddon(k0, k1)
+                rows = (k1 - k0) * n
+                cnt = torch.empty(rows, dtype=torch.int64, device=self.dev)
+                _lib.call("xct_csr_filter_cols", ip.data_ptr(), ix.data_ptr(), v.data_ptr(),
+                          rows, lo, hi, cnt.data_ptr(), None, None, None, st)
+                optr = torch.zeros(rows + 1, dtype=torch.int64, device=self.dev)
+                torch.cumsum(cnt, 0, out=optr[1:])
+                m = int(optr[-1])
+                oi = torch.empty(max(m, 1), dtype=torch.int32, device=self.dev)
+                ov = torch.empty(max(m, 1), dtype=torch.float64, device=self.dev)
+                _lib.call("xct_csr_filter_cols", ip.data_ptr(), ix.data_ptr(), v.data_ptr(),
+                          rows, lo, hi, None, optr.data_ptr(), oi.data_ptr(), ov.data_ptr(), st)
+                counts.append(cnt.cpu().numpy())
+                idx.append(oi[:m].cpu().numpy())
+                val.append(ov[:m].cpu().numpy())
+            bip = np.zeros(R + 1, np.int64)
+            np.cumsum(np.concatenate(counts), out=bip[1:])
+            bix, bv = np.concatenate(idx), np.concatenate(val)
+            del counts, idx, val
+            t_ip, t_ix, t_v = _transpose(bip, bix, bv, R, hi - lo)
+            del bip, bix, bv
+            plan = matrixstore.adjoint_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, z0, z1)
+            plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - lo, -1).astype(np.int32)
+            hf = matrixstore.build_format(t_ip, t_ix, t_v, hi - lo, R, plan, cfg.precision,
+                                          cfg.ffactor, exp, cfg.smem_budget,
+                                          schedule=cfg.order == "native")
+            hf.cta_rows = np.where(hf.cta_rows >= 0, hf.cta_rows + lo, -1).astype(np.int32)
+            parts.append(hf)
+        hf = matrixstore.concat_formats(parts)
+        del parts
+        return matrixstore.upload_format(hf, cfg.precision, cfg.ffactor, R, g.num_voxels, exp,
+                                         self.dev)
+
+    def run(self) -> AssembledSystem:
+        import torch
+        from .parallel import MatrixInfo
+        cfg, g = self.cfg, self.g
+        ta = matrixstore.forward_tile_height(g.grid_n, self.rw, cfg.warps_per_cta)
+        chunks = self._chunks(ta)
+        exp = self._exponent(chunks) if cfg.precision in ("half", "mixed") else 0
+        self.nnz = 0
+        fwd = self._forward(exp)
+        torch.cuda.empty_cache()
+        adj = self._adjoint(exp, chunks)
+        torch.cuda.empty_cache()
+        info = MatrixInfo(g.num_rays, g.num_voxels, self.nnz, g.num_angles, g.num_detector_cols)
+        return AssembledSystem.from_sides(info, cfg, g, fwd, adj, exp)
