@@ -42,8 +42,10 @@ CONFIGS = {
                desc="1024x1024, 1024 angles, 256 slices per GPU, FP32 CG"),
     "c2m": dict(n=1024, k=1024, slices=256, precision="mixed", iters=50,
                 desc="1024x1024, 1024 angles, 256 slices per GPU, FP16 storage"),
-    "c5": dict(n=2048, k=2048, slices=1024, precision="mixed", iters=30,
-               desc="2048x2048, 2048 angles, 1024 slices, FP16 storage"),
+    "c5": dict(n=2048, k=2048, slices=1024, precision="mixed", iters=30, strong=True,
+               desc="2048x2048, 2048 angles, 1024 slices total, FP16 storage"),
+    "c3": dict(n=1024, k=1024, slices=2048, precision="single", iters=50, strong=True,
+               desc="1024x1024, 1024 angles, 2048 slices total, slice batch, FP32"),
 }
 
 
@@ -111,17 +113,15 @@ class ClockSampler:
                 else None, "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_problem(cfg, slices, dev):
+def make_problem(cfg, slices):
     """Shepp-Logan phantom (identical slices, src/geometry.py:337-339) and
-    y = A x computed on the device in float64."""
-    import torch
-    from paper_2009_07226_b200 import engine, geometry
+    y = A x in float64 on the device (Siddon streamed over view chunks).
+    Returns the one distinct sinogram column; the (rays, slices) problem is
+    a zero-stride host view of it."""
+    from paper_2009_07226_b200 import geometry
     g = geometry.make_geometry(cfg["k"], slices, cfg["n"])
-    A = geometry.build_system_matrix(g)
     ph = geometry.generate_phantom("shepp-logan-like", cfg["n"], 1).slices_as_columns()
-    y1 = engine.csr_spmm_f64(A, ph.astype(np.float64))          # (rays, 1)
-    y = torch.from_numpy(np.ascontiguousarray(y1)).to(dev).repeat(1, slices).contiguous()
-    return g, A, y
+    return g, geometry.project_f64(g, ph.astype(np.float64))     # (rays, 1)
 
 
 def cpu_baseline(cfg, slices, sample_angles=16, sample_slices=16):
@@ -162,18 +162,20 @@ def run_reference_arm(args, cfg, ws, rank):
     from paper_2009_07226_b200 import geometry
     g = geometry.make_geometry(cfg["k"], cfg["slices"], cfg["n"])
     nnz_full = int(round(1.1954 * cfg["k"] * cfg["n"] ** 2))
+    total = cfg["slices"] if cfg.get("strong") else cfg["slices"] * ws
     times = []
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline(cfg, cfg["slices"] * ws)
+        r = cpu_baseline(cfg, total)
         if i >= args.warmup:
             times.append(r["t_iter_extrap"])
     nnz_full = int(round(r["nnz_sample"] * cfg["k"] / r["kp"]))
     t = statistics.median(times)
-    gflops = 4.0 * nnz_full * cfg["slices"] * ws / t / 1e9
+    gflops = 4.0 * nnz_full * total / t / 1e9
     del g
     line = {"impl": "reference", "metric": metric_name(cfg), "value": gflops, "unit": "GFLOPS",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong" if cfg.get("strong") else "weak",
             "vs_baseline": None, "dtype": "f32" if cfg["precision"] == "single" else "f16/f32",
             "data": "synthetic", "config": config_block(cfg, ws),
             "cg_s_per_iter": t,
@@ -192,8 +194,10 @@ def metric_name(cfg):
 
 
 def config_block(cfg, ws):
+    total = cfg["slices"] if cfg.get("strong") else cfg["slices"] * ws
     return {"workload": cfg["desc"], "n": cfg["n"], "angles": cfg["k"],
-            "slices_per_gpu": cfg["slices"], "total_slices": cfg["slices"] * ws,
+            "slices_per_gpu": cfg["slices"] if not cfg.get("strong") else -(-total // ws),
+            "total_slices": total,
             "precision": cfg["precision"], "ffactor": 16, "step": "one CGLS iteration",
             "parallelism": f"slice-batch P_b={ws}", "l2": "inputs >> L2 (matrix "
             "streamed from HBM every application), no flush needed"}
@@ -229,30 +233,35 @@ def main():
 
     from paper_2009_07226_b200 import parallel
     scfg = pipeline.SystemConfig(precision=cfg["precision"], ffactor=16, order=args.order)
+    # slices on this rank: weak scaling = a fixed group per GPU; strong
+    # scaling = the config's total split by the reference's P_b rule
+    if cfg.get("strong"):
+        lo, hi = parallel.slice_groups(cfg["slices"], ws)[rank]
+        S = hi - lo
+    else:
+        S = cfg["slices"]
     t0 = time.perf_counter()
     system, t_matrix = None, 0.0
     if rank == 0:
-        g, A, y = make_problem(cfg, cfg["slices"], dev)
+        g, y1 = make_problem(cfg, S)
         t_matrix = time.perf_counter() - t0
         system = pipeline.assemble(g, scfg)
         geometry.clear_matrix_cache()
-        A.release_device()                   # keep HBM for the run
         torch.cuda.empty_cache()
     else:
-        g = geometry.make_geometry(cfg["k"], cfg["slices"], cfg["n"])
+        g = geometry.make_geometry(cfg["k"], S, cfg["n"])
     if ws > 1:
         # one host build; the staged operator goes to every GPU over NVLink
         system = parallel.broadcast_system(system, scfg, g)
-        y1 = [y[:, :1].contiguous() if rank == 0 else None]
-        yt = y1[0] if rank == 0 else torch.empty((g.num_rays, 1), dtype=torch.float64,
-                                                  device=dev)
+        yt = (torch.from_numpy(y1).to(dev) if rank == 0 else
+              torch.empty((g.num_rays, 1), dtype=torch.float64, device=dev))
         dist.broadcast(yt, src=0)
-        y = yt.repeat(1, cfg["slices"]).contiguous()
+        y1 = yt.cpu().numpy()
+    y = np.broadcast_to(y1, (g.num_rays, S))      # identical phantom slices
     torch.cuda.synchronize()
     t_assemble = time.perf_counter() - t0 - t_matrix
     nnz = system.matrix.nnz
 
-    S = cfg["slices"]
     W, K = max(args.warmup, 0), max(args.steps, 1)
     run = solver.CGLSRun(system, y, solver.SolveConfig(max_iters=W + K + 1,
                                                        precision=cfg["precision"]))
@@ -284,7 +293,8 @@ def main():
         t_max = float(tt.item())
     t_iter = t_max / K
     flops_iter = 4.0 * nnz * S            # forward + adjoint, 2 flops per nnz per slice
-    value = flops_iter * ws / t_iter / 1e9
+    S_total = cfg["slices"] if cfg.get("strong") else cfg["slices"] * ws
+    value = 4.0 * nnz * S_total / t_iter / 1e9
 
     # roofline of the staged SpMM (compulsory bytes)
     from paper_2009_07226_b200 import matrixstore
@@ -308,7 +318,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         iters = args.e2e_iters or min(cfg["iters"], 10)
-        y_host = y.cpu().pin_memory()
+        y_host = torch.from_numpy(np.ascontiguousarray(y)).pin_memory()
         del run
         torch.cuda.empty_cache()
         if ws > 1:
@@ -324,7 +334,7 @@ def main():
             tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
-        e2e = {"value": flops_iter * res.iterations * ws / t_e2e / 1e9, "unit": "GFLOPS",
+        e2e = {"value": 4.0 * nnz * S_total * res.iterations / t_e2e / 1e9, "unit": "GFLOPS",
                "h2d_bytes_per_step": int(y_host.numel() * 8),
                "d2h_bytes_per_step": int(x_host.numel() * 8),
                "step": f"one cgls_solve({iters} iterations) call with host arrays",
@@ -344,13 +354,13 @@ def main():
         line = {
             "metric": metric_name(cfg), "value": value, "unit": "GFLOPS", "n_gpus": ws,
             "steps": K, "warmup": W, "ms_per_step": t_iter * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None,
             "dtype": "f32" if cfg["precision"] == "single" else
                      ("f16 storage / f32 accumulate" if cfg["precision"] == "mixed"
                       else cfg["precision"]),
             "data": "synthetic Shepp-Logan phantom, y = A x (float64, on device)",
             "config": config_block(cfg, ws),
-            "cg_s_per_iter": t_iter, "voxels_per_s": C * S * ws / t_iter,
+            "cg_s_per_iter": t_iter, "voxels_per_s": C * S_total / t_iter,
             "spmm_gflops_kernel": spmm_gflops, "spmm_launches_timed": n_spmm,
             "nnz": nnz, "assemble_s": t_assemble, "matrix_build_s": t_matrix,
             "operator_hbm_bytes": system.hbm_bytes(),

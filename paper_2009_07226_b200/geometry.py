@@ -348,3 +348,27 @@ def simulate_measurements(matrix: SystemMatrix, tomogram: Volume, noise_sigma: f
         y = y + rng.normal(0.0, noise_sigma * y.max(), size=y.shape)
     data = y.T.reshape(tomogram.num_slices, matrix.num_angles, matrix.num_detector_cols)
     return Volume(np.ascontiguousarray(data), role="sinogram")
+
+
+def project_f64(geometry: ScanGeometry, x: np.ndarray, chunk_nnz: float = 4e8) -> np.ndarray:
+    """y = A x in float64 without holding A: Siddon regenerated per chunk of
+    views on the device, each chunk multiplied by K-CSR-f64 (used for large
+    geometries where build_system_matrix would not fit)."""
+    import torch
+    dev = device()
+    X = np.ascontiguousarray(x.reshape(x.shape[0], -1), np.float64)
+    d_x = torch.from_numpy(X).to(dev)
+    n = geometry.grid_n
+    per = max(1, int(chunk_nnz // (1.2 * n * n)))
+    out = np.empty((geometry.num_rays, X.shape[1]))
+    st = _lib.stream_handle(dev)
+    for k0 in range(0, geometry.num_angles, per):
+        k1 = min(geometry.num_angles, k0 + per)
+        ip, ix, v = siddon_csr(geometry, k0, k1, dev)
+        rows = (k1 - k0) * n
+        y = torch.empty((rows, X.shape[1]), dtype=torch.float64, device=dev)
+        _lib.call("xct_csr_spmm_f64", ip.data_ptr(), ix.data_ptr() if ix.numel() else None,
+                  v.data_ptr() if v.numel() else None, rows, d_x.data_ptr(), X.shape[1],
+                  y.data_ptr(), st)
+        out[k0 * n:k1 * n] = y.cpu().numpy()
+    return out.reshape(geometry.num_rays) if x.ndim == 1 else out

@@ -458,38 +458,89 @@ def concat_formats(parts: list) -> HostFormat:
     return HostFormat(arrays, info, np.concatenate(rows), parts[0].plan_kind)
 
 
-def upload_format(hf: HostFormat, precision: str, ffactor: int, n_in: int, n_out: int,
+def upload_format(hf, precision: str, ffactor: int, n_in: int, n_out: int,
                   value_scale_exp: int, dev=None) -> "DeviceSide":
-    """Encode the entries for K6 and move the format to HBM."""
+    """Encode the entries for K6 and move the format (a HostFormat or a list
+    of parts over disjoint CTA tiles) to HBM.  Parts are rebased and copied
+    straight into the final device arrays, in bounded host blocks, so no
+    whole-operator host copy is ever made."""
     import torch
     from .geometry import device
     dev = dev or device()
-    h = dict(hf.arrays)
+    parts = hf if isinstance(hf, list) else [hf]
+    i0 = parts[0].info
+    for p in parts:
+        for k in ("rows_per_cta", "rows_per_warp", "warps_per_cta", "value_bytes"):
+            if p.info[k] != i0[k]:
+                raise ValueError(f"cannot combine formats with different {k}")
+    tot = {k: sum(int(p.info[k]) for p in parts)
+           for k in ("n_cta", "n_groups", "n_slots", "n_padded", "nnz", "underflow_count")}
+    info = _lib.FormatInfo()
+    for f, v in i0.items():
+        setattr(info, f, v)
+    for k, v in tot.items():
+        setattr(info, k, v)
+    info.max_group_slots = max(int(p.info["max_group_slots"]) for p in parts)
+    info.max_rel_quant_error = max(float(p.info["max_rel_quant_error"]) for p in parts)
     f_dev = f_dev_for(ffactor, precision)
     # K6 addresses a staged record by its byte offset inside a plane
-    plane_slots = -(-int(hf.info["max_group_slots"]) // 8) * 8
+    plane_slots = -(-int(info.max_group_slots) // 8) * 8
     if plane_slots * 16 > 65536:
         raise StageSplitRequired("load group too large for 16-bit plane offsets")
-    h["slots"] = (h["slots"].astype(np.uint32) << 4).astype(np.uint16)
-    if precision in ("half", "mixed"):
-        # one 32-bit word per entry: byte offset << 16 | fp16 length
-        h["values"] = ((h["slots"].astype(np.uint32) << 16) |
-                       h["values"].view(np.uint16)).view(np.int32)
-        h["slots"] = np.zeros(1, np.uint16)
-    # the kernel's load ring reads up to 4 steps (x 32 rows x 4) past a slab
-    for k in ("slots", "values"):
-        h[k] = np.concatenate([h[k], np.zeros(1024, h[k].dtype)])
-    for k in ("group_map", "slab_off", "slab_width"):
-        if len(h[k]) == 0:
-            h[k] = np.zeros(1, h[k].dtype)
-    t = {k: torch.from_numpy(v.view(np.int16) if v.dtype == np.uint16 else v).to(dev)
-         for k, v in h.items()}
-    t["cta_rows"] = torch.from_numpy(np.ascontiguousarray(hf.cta_rows, np.int32)).to(dev)
-    info = _lib.FormatInfo()
-    for f, v in hf.info.items():
-        setattr(info, f, v)
-    side = DeviceSide(precision, ffactor, f_dev, n_in, n_out, value_scale_exp, info, t,
-                      plan_kind=hf.plan_kind)
+    packed = precision in ("half", "mixed")
+    warps = int(info.warps_per_cta)
+    pad = 1024          # the kernel's load ring reads up to 4 steps past a slab
+    T = {}
+
+    def alloc(name, n, dtype):
+        T[name] = torch.zeros(max(int(n), 1), dtype=dtype, device=dev)
+    alloc("cta_group_ptr", tot["n_cta"] + 1, torch.int32)
+    alloc("group_map_ptr", tot["n_groups"] + 1, torch.int64)
+    alloc("group_map", tot["n_slots"], torch.int32)
+    alloc("slab_off", tot["n_groups"] * warps, torch.int64)
+    alloc("slab_width", tot["n_groups"] * warps, torch.int32)
+    alloc("cta_rows", tot["n_cta"] * int(info.rows_per_cta), torch.int32)
+    if packed:
+        alloc("values", tot["n_padded"] + pad, torch.int32)
+        alloc("slots", 1, torch.int16)
+    else:
+        alloc("values", tot["n_padded"] + pad,
+              torch.float64 if precision == "double" else torch.float32)
+        alloc("slots", tot["n_padded"] + pad, torch.int16)
+
+    def put(name, at, arr):
+        if len(arr):
+            T[name][at:at + len(arr)].copy_(torch.from_numpy(np.ascontiguousarray(arr)))
+
+    c_off = g_off = s_off = e_off = r_off = 0
+    block = 1 << 26
+    for p in parts:
+        a, inf = p.arrays, p.info
+        put("cta_group_ptr", c_off, a["cta_group_ptr"][:-1] + g_off)
+        put("group_map_ptr", g_off, a["group_map_ptr"][:-1] + s_off)
+        put("group_map", s_off, a["group_map"])
+        put("slab_off", g_off * warps, a["slab_off"] + e_off)
+        put("slab_width", g_off * warps, a["slab_width"])
+        put("cta_rows", r_off, p.cta_rows)
+        n = int(inf["n_padded"])
+        for b0 in range(0, n, block):
+            b1 = min(n, b0 + block)
+            off = a["slots"][b0:b1].astype(np.uint32) << 4
+            if packed:
+                word = (off << 16) | a["values"][b0:b1].view(np.uint16)
+                put("values", e_off + b0, word.view(np.int32))
+            else:
+                put("slots", e_off + b0, off.astype(np.uint16).view(np.int16))
+                put("values", e_off + b0, a["values"][b0:b1])
+        c_off += int(inf["n_cta"])
+        g_off += int(inf["n_groups"])
+        s_off += int(inf["n_slots"])
+        e_off += n
+        r_off += len(p.cta_rows)
+    T["cta_group_ptr"][tot["n_cta"]] = g_off
+    T["group_map_ptr"][tot["n_groups"]] = s_off
+    side = DeviceSide(precision, ffactor, f_dev, n_in, n_out, value_scale_exp, info, T,
+                      plan_kind=parts[0].plan_kind)
     return attach(side)
 
 

@@ -469,9 +469,7 @@ class StreamedAssembly:
             hf.cta_rows = np.where(hf.cta_rows >= 0, hf.cta_rows + base, -1).astype(np.int32)
             parts.append(hf)
             self.nnz += int(hf.info["nnz"])
-        hf = matrixstore.concat_formats(parts)
-        del parts
-        return matrixstore.upload_format(hf, cfg.precision, cfg.ffactor, g.num_voxels,
+        return matrixstore.upload_format(parts, cfg.precision, cfg.ffactor, g.num_voxels,
                                          g.num_rays, exp, self.dev)
 
     def _adjoint(self, exp, chunks):
@@ -516,10 +514,8 @@ class StreamedAssembly:
                                           schedule=cfg.order == "native")
             hf.cta_rows = np.where(hf.cta_rows >= 0, hf.cta_rows + lo, -1).astype(np.int32)
             parts.append(hf)
-        hf = matrixstore.concat_formats(parts)
-        del parts
-        return matrixstore.upload_format(hf, cfg.precision, cfg.ffactor, R, g.num_voxels, exp,
-                                         self.dev)
+        return matrixstore.upload_format(parts, cfg.precision, cfg.ffactor, R, g.num_voxels,
+                                         exp, self.dev)
 
     def run(self) -> AssembledSystem:
         import torch
@@ -530,6 +526,8 @@ class StreamedAssembly:
         exp = self._exponent(chunks) if cfg.precision in ("half", "mixed") else 0
         self.nnz = 0
         fwd = self._forward(exp)
+        import gc
+        gc.collect()
         torch.cuda.empty_cache()
         adj = self._adjoint(exp, chunks)
         torch.cuda.empty_cache()

@@ -283,35 +283,76 @@ class CGLSRun:
         self.done = False
 
     def start(self) -> bool:
+        """Setup and the initial back projection (src/solver.py:141-157).
+        y is streamed one F-chunk of slices at a time (host or device), so
+        no full-size float64/float32 copy of the measurements is ever made
+        on the device: pass 1 reduces max|wd(y)| and ||y||^2, pass 2 writes
+        the stored residual r = store(wd(y))."""
         import torch
         cg, prec, system = self.cg, self.config.precision, self.system
         S, n_rows, n_cols = cg.S, system.num_rows, system.num_cols
-        Y = torch.as_tensor(self.y, device=cg.dev)
-        if Y.dtype != torch.float64:
-            Y = Y.to(torch.float64)
-        Y = Y.reshape(n_rows, S).contiguous()
-        cg.bits.zero_()
-        _lib.call("xct_maxabs", Y.data_ptr(), 0, Y.numel(), 1.0, cg.bits.data_ptr(), cg.st)
-        if not math.isfinite(float(cg.bits[:1].cpu().numpy().view(np.float64)[0])):
+        y = self.y
+        if isinstance(y, np.ndarray):
+            y = y.reshape(n_rows, S)
+        else:
+            y = y.reshape(n_rows, S)
+
+        def chunk(c):
+            lo, hi = c * cg.F, min(S, (c + 1) * cg.F)
+            yc = y[:, lo:hi]
+            if isinstance(yc, np.ndarray):
+                yc = torch.from_numpy(np.ascontiguousarray(yc, dtype=np.float64))
+            return yc.to(device=cg.dev, dtype=torch.float64).contiguous(), hi - lo
+
+        per = n_rows * cg.f_dev
+        tmp = torch.empty(per, dtype=cg.wdt, device=cg.dev)
+        if cg.reduced:
+            r = _Vec(torch.empty(cg.numel(n_rows), dtype=torch.float16, device=cg.dev), 2, 1.0)
+        else:
+            r = _Vec(torch.empty(cg.numel(n_rows), dtype=cg.wdt, device=cg.dev), cg.code)
+        ybits = torch.zeros(1, dtype=torch.int64, device=cg.dev)
+        rbits = torch.zeros(1, dtype=torch.int64, device=cg.dev)
+        y_sq = 0.0
+        for c in range(cg.n_chunks):
+            yc, w = chunk(c)
+            _lib.call("xct_maxabs", yc.data_ptr(), 0, yc.numel(), 1.0, ybits.data_ptr(), cg.st)
+            _lib.call("xct_dot", yc.data_ptr(), yc.data_ptr(), 0, yc.numel(), 1.0, 1.0,
+                      cg.scratch.data_ptr(), cg.scal.data_ptr(), cg.st)
+            y_sq += float(cg.scal[0].item())
+            dst = tmp if cg.reduced else r.t[c * per:(c + 1) * per]
+            _lib.call("xct_chunk_from_f64", yc.data_ptr(), n_rows, w, cg.F, cg.f_dev, cg.code,
+                      dst.data_ptr(), cg.st)
+            if cg.reduced:
+                _lib.call("xct_maxabs", tmp.data_ptr(), 1, per, 1.0, rbits.data_ptr(), cg.st)
+        if not math.isfinite(float(ybits.cpu().numpy().view(np.float64)[0])):
             raise SolverDivergence(0, prec, "measurement data contains NaN or Inf")
-        _lib.call("xct_dot", Y.data_ptr(), Y.data_ptr(), 0, Y.numel(), 1.0, 1.0,
-                  cg.scratch.data_ptr(), cg.scal.data_ptr(), cg.st)
-        self.y_norm = math.sqrt(float(cg.scal[0].item()))
+        self.y_norm = math.sqrt(y_sq)
         if self.y_norm == 0.0:
             self.done = True
             self.x = None
             return False
         if cg.reduced:
+            peak = float(rbits.cpu().numpy().view(np.float64)[0])
+            r.factor = peak if peak > 0 else 1.0
+            f32 = float(np.float32(r.factor))
+            for c in range(cg.n_chunks):
+                yc, w = chunk(c)
+                _lib.call("xct_chunk_from_f64", yc.data_ptr(), n_rows, w, cg.F, cg.f_dev, 1,
+                          tmp.data_ptr(), cg.st)
+                _lib.call("xct_axpy", tmp.data_ptr(), 1, 1.0, None, 1, 1.0, 0.0, per,
+                          r.t[c * per:(c + 1) * per].data_ptr(), 2, f32, None,
+                          cg.scratch.data_ptr(), None, cg.st)
+        del tmp
+        self.r = r
+        if cg.reduced:
             self.x = _Vec(torch.zeros(cg.numel(n_cols), dtype=torch.float16, device=cg.dev), 2, 1.0)
         else:
             self.x = _Vec(torch.zeros(cg.numel(n_cols), dtype=cg.wdt, device=cg.dev), cg.code)
-        r_work = cg.empty(n_rows)
-        _lib.call("xct_chunk_from_f64", Y.data_ptr(), n_rows, S, cg.F, cg.f_dev, cg.code,
-                  r_work.data_ptr(), cg.st)
-        del Y
-        self.r = cg.store(r_work)
-        self.s_buf = torch.empty(cg.numel(n_cols), dtype=cg.out_dt, device=cg.dev)
-        self.q_buf = torch.empty(cg.numel(n_rows), dtype=cg.out_dt, device=cg.dev)
+        # one output buffer serves q (projection) and s (back projection):
+        # q is dead once r is updated, s is produced after that
+        buf = torch.empty(cg.numel(max(n_rows, n_cols)), dtype=cg.out_dt, device=cg.dev)
+        self.s_buf = buf[:cg.numel(n_cols)]
+        self.q_buf = buf[:cg.numel(n_rows)]
         facs, gamma = cg.apply(system.adjoint, self.r, self.s_buf)
         if facs is None:
             raise SolverDivergence(0, prec, "residual contains NaN or Inf")
