@@ -326,20 +326,25 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
   }
   std::vector<int64_t> cta_slot0(n_cta + 1, 0);
   {
+    // a warp's slabs of all groups of its tile are contiguous ([tile][warp]
+    // [group]): the kernel streams them as one strided sequence, prefetching
+    // across group boundaries
     int64_t gi = 0, so = 0, eo = 0;
     for (int64_t b = 0; b < n_cta; ++b) {
       cta_slot0[b] = so;
       const CtaPlan& P = plans[b];
       int64_t ng = P.gstart.empty() ? 0 : (int64_t)P.gstart.size() - 1;
-      for (int64_t g = 0; g < ng; ++g, ++gi) {
+      for (int64_t g = 0; g < ng; ++g) {
         so += P.gstart[g + 1] - P.gstart[g];
-        F->group_map_ptr[gi + 1] = so;
-        for (int64_t w = 0; w < warps; ++w) {
-          F->slab_off[gi * warps + w] = eo;
-          F->slab_width[gi * warps + w] = P.width[g * warps + w];
+        F->group_map_ptr[gi + g + 1] = so;
+      }
+      for (int64_t w = 0; w < warps; ++w)
+        for (int64_t g = 0; g < ng; ++g) {
+          F->slab_off[(gi + g) * warps + w] = eo;
+          F->slab_width[(gi + g) * warps + w] = P.width[g * warps + w];
           eo += (int64_t)P.width[g * warps + w] * rows_per_warp;
         }
-      }
+      gi += ng;
     }
   }
 

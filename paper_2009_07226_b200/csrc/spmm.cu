@@ -313,11 +313,25 @@ __global__ void __launch_bounds__(1024) spmm_staged_kernel(const Params p) {
   A acc;
   acc.zero();
   const int g0 = p.cta_group_ptr[b], g1 = p.cta_group_ptr[b + 1];
+  // The warp's slabs of all groups are contiguous, so its entries form one
+  // strided stream across groups: the register ring is filled once and keeps
+  // kDepth steps in flight straight through the group boundaries.
+  const int64_t step = (int64_t)rpw * 4;
+  int64_t at = (g0 < g1 ? p.slab_off[(int64_t)g0 * p.warps_per_cta + warp] : 0) +
+               (int64_t)rin * 4;
+  St r0, r1, r2, r3;
+  r0.load(p.slots, p.values, at, pol_e);
+  r1.load(p.slots, p.values, at + step, pol_e);
+  r2.load(p.slots, p.values, at + 2 * step, pol_e);
+  r3.load(p.slots, p.values, at + 3 * step, pol_e);
+  at += 4 * step;
+  int t = 0;                               // steps consumed so far (ring phase)
   // two stage buffers: group g+1 is staged while group g is consumed
   if (g0 < g1) stage_fill(p, xb, s0, g0, lp, pol_x);
   cp_async_commit();
   for (int g = g0; g < g1; ++g) {
     const uint32_t cur_buf = s0 + (((g - g0) & 1) ? bb : 0u);
+    const int n4 = p.slab_width[(int64_t)g * p.warps_per_cta + warp] >> 2;
     cp_async_wait_all();
     __syncthreads();                     // fill(g) visible; everyone done with g-1
     if (g + 1 < g1) stage_fill(p, xb, s0 + (((g - g0) & 1) ? 0u : bb), g + 1, lp, pol_x);
@@ -326,31 +340,28 @@ __global__ void __launch_bounds__(1024) spmm_staged_kernel(const Params p) {
     uint32_t pb[NPL];
 #pragma unroll
     for (int qq = 0; qq < NPL; ++qq) pb[qq] = cur_buf + pbase[qq];
-    const int64_t off = p.slab_off[(int64_t)g * p.warps_per_cta + warp];
-    const int n4 = p.slab_width[(int64_t)g * p.warps_per_cta + warp] >> 2;
-    const int64_t step = (int64_t)rpw * 4;
-    int64_t at = off + (int64_t)rin * 4;
-    // ring of kDepth steps; a slot is refilled right after it is consumed.
-    // The entry arrays are padded so prefetching past a slab end is safe.
-    St r0, r1, r2, r3;
-    r0.load(p.slots, p.values, at, pol_e);
-    r1.load(p.slots, p.values, at + step, pol_e);
-    r2.load(p.slots, p.values, at + 2 * step, pol_e);
-    r3.load(p.slots, p.values, at + 3 * step, pol_e);
-    at += 4 * step;
-    for (int k = 0; k < n4; k += kDepth) {
-      consume<PREC, NPL>(acc, r0, pb);
-      r0.load(p.slots, p.values, at, pol_e);
-      if (k + 1 >= n4) break;
-      consume<PREC, NPL>(acc, r1, pb);
-      r1.load(p.slots, p.values, at + step, pol_e);
-      if (k + 2 >= n4) break;
-      consume<PREC, NPL>(acc, r2, pb);
-      r2.load(p.slots, p.values, at + 2 * step, pol_e);
-      if (k + 3 >= n4) break;
-      consume<PREC, NPL>(acc, r3, pb);
-      r3.load(p.slots, p.values, at + 3 * step, pol_e);
-      at += 4 * step;
+    const int end = t + n4;
+    while (t < end) {
+      switch (t & 3) {
+        case 0:
+          consume<PREC, NPL>(acc, r0, pb);
+          r0.load(p.slots, p.values, at, pol_e);
+          break;
+        case 1:
+          consume<PREC, NPL>(acc, r1, pb);
+          r1.load(p.slots, p.values, at, pol_e);
+          break;
+        case 2:
+          consume<PREC, NPL>(acc, r2, pb);
+          r2.load(p.slots, p.values, at, pol_e);
+          break;
+        default:
+          consume<PREC, NPL>(acc, r3, pb);
+          r3.load(p.slots, p.values, at, pol_e);
+          break;
+      }
+      at += step;
+      ++t;
     }
   }
   cp_async_wait_all();
