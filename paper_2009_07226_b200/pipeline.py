@@ -49,6 +49,9 @@ class SystemConfig:
                      to the reference's default configuration.
       warps_per_cta  CTA size of the staged SpMM.
       smem_budget    shared-memory bytes per CTA for one load group.
+      pieces_per_lane  16-byte pieces of a staged record each lane owns (1, 2
+                     or 4; lanes per row = record pieces / this; None = up
+                     to 4: one lane per row for FP16/FP32 at F=16).
       build          "streamed": never materialize the whole matrix -- the
                      projection format is built per chunk of views, the back
                      projection per band of voxels, from Siddon regenerated
@@ -71,6 +74,7 @@ class SystemConfig:
     warps_per_cta: int = 16
     smem_budget: int = matrixstore.SMEM_BUDGET
     build: str = "auto"
+    pieces_per_lane: int | None = None
 
     def __post_init__(self):
         if self.precision not in matrixstore.PRECISIONS:
@@ -100,7 +104,8 @@ class _Side:
 
 
 def _rows_per_warp(cfg) -> int:
-    return 32 // matrixstore.lanes_for(cfg.ffactor, cfg.precision)
+    ppl = cfg.pieces_per_lane or 4
+    return 32 // matrixstore.lanes_for(cfg.ffactor, cfg.precision, ppl)
 
 
 def _csr_host(matrix):

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--smem", type=int, default=96 * 1024)
     ap.add_argument("--slices", type=int, default=None)
     ap.add_argument("--order", default="native")
+    ap.add_argument("--ppl", type=int, default=None)
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.precision:
@@ -43,7 +44,7 @@ def main():
     t0 = time.perf_counter()
     system = pipeline.assemble(g, pipeline.SystemConfig(
         precision=cfg["precision"], ffactor=16, order=args.order, warps_per_cta=args.warps,
-        smem_budget=args.smem))
+        smem_budget=args.smem, pieces_per_lane=args.ppl))
     t_asm = time.perf_counter() - t0
     nnz = system.matrix.nnz
     geometry.clear_matrix_cache()
@@ -53,7 +54,7 @@ def main():
     od = torch.float64 if prec == "double" else torch.float32
     eb = matrixstore.element_bytes(prec)
     out = {"config": args.config, "precision": prec, "slices": S, "nnz": nnz,
-           "assemble_s": t_asm, "warps": args.warps, "smem": args.smem}
+           "assemble_s": t_asm, "warps": args.warps, "smem": args.smem, "ppl": args.ppl}
     for name, side in (("forward", system.forward), ("adjoint", system.adjoint)):
         blk = side.blocks[0]
         n_chunks = -(-S // 16)
