@@ -240,6 +240,25 @@ int xct_chunk_from_f64(const double* d_in, int64_t n, int64_t n_slices,
                        int32_t ffactor, int32_t f_dev, int out_dtype,
                        void* d_out, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * K10  partial-result exchange of the data-partitioned operator
+ * replaces comm.execute_plan / engine.reduce_partials (src/comm.py:420-472,
+ * src/engine.py:189-221).  Chunked vectors [n_chunks][n][fd] (f32, or f64
+ * when f64 != 0); whole element rows move.  The caller fixes the summation
+ * order (owner's own partial first, then senders ascending = the
+ * reference's direct plan); the bytes travel with NCCL over NVLink.
+ * ------------------------------------------------------------------------- */
+/* dst[c][i] = src[c][idx[i]] */
+int xct_gather_rows(const void* d_src, int64_t n_src, const int32_t* d_idx, int64_t m,
+                    int64_t n_chunks, int32_t fd, int f64, void* d_dst, void* stream);
+/* dst[c][pos[i]] += src[c][i] */
+int xct_accumulate_rows(void* d_dst, int64_t n_dst, const void* d_src, const int32_t* d_pos,
+                        int64_t m, int64_t n_chunks, int32_t fd, int f64, void* stream);
+/* v[c][*] *= factors[c] (denormalize, src/matrixstore.py:308-316) and, if
+ * d_sumsq, the f64 sum of squares of the result (d_scratch[148*8]) */
+int xct_scale_chunks(void* d_v, int64_t per_chunk, int64_t n_chunks, const double* d_factors,
+                     int f64, double* d_scratch, double* d_sumsq, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,9 @@ _SIGS = {
     "xct_normalize_chunked": (i32, [vp, i32, f32, i64, i64, i32, vp, i32, vp, vp]),
     "xct_unchunk_f64": (i32, [vp, i32, f32, i64, i64, i32, i32, vp, vp]),
     "xct_chunk_from_f64": (i32, [vp, i64, i64, i32, i32, i32, vp, vp]),
+    "xct_gather_rows": (i32, [vp, i64, vp, i64, i64, i32, i32, vp, vp]),
+    "xct_accumulate_rows": (i32, [vp, i64, vp, vp, i64, i64, i32, i32, vp]),
+    "xct_scale_chunks": (i32, [vp, i64, i64, vp, i32, vp, vp, vp]),
 }
 
 _lib = None
@@ -118,7 +121,8 @@ KERNELS_PER_CALL = {"xct_dot": 2, "xct_sum_f64": 1, "xct_spmm": 1, "xct_maxabs":
                     "xct_chunk_maxabs": 1, "xct_normalize": 1, "xct_chunk_maxabs_chunked": 1,
                     "xct_normalize_chunked": 1, "xct_unchunk_f64": 1, "xct_chunk_from_f64": 1,
                     "xct_csr_spmm_f64": 1, "xct_siddon_count": 1, "xct_siddon_fill": 1,
-                    "xct_csr_filter_cols": 1}
+                    "xct_csr_filter_cols": 1, "xct_gather_rows": 1,
+                    "xct_accumulate_rows": 1, "xct_scale_chunks": 2}
 launch_count = [0]
 
 

@@ -410,3 +410,96 @@ extern "C" int xct_sum_f64(const double* d_v, int64_t n, double* d_result, void*
   XCT_CUDA_CHECK_LAUNCH("sum_f64");
   return XCT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// K10: partial-result exchange helpers for the data-partitioned operator
+// (comm.execute_plan / engine.reduce_partials, src/comm.py:420-472,
+// src/engine.py:189-221).  Vectors are chunked [n_chunks][n][fd]; element
+// rows are moved whole (fd values).  All ops are plain elementwise f32/f64,
+// order fixed by the caller (owner first, then senders ascending).
+namespace {
+template <typename T>
+__global__ void gather_rows_k(const T* src, int64_t n_src, const int32_t* idx, int64_t m,
+                              int64_t n_chunks, int fd, T* dst) {
+  const int64_t total = n_chunks * m * fd;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / (m * fd), rem = t % (m * fd);
+    const int64_t i = rem / fd, f = rem % fd;
+    dst[t] = src[(c * n_src + idx[i]) * fd + f];
+  }
+}
+template <typename T>
+__global__ void accumulate_rows_k(T* dst, int64_t n_dst, const T* src, const int32_t* pos,
+                                  int64_t m, int64_t n_chunks, int fd) {
+  const int64_t total = n_chunks * m * fd;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / (m * fd), rem = t % (m * fd);
+    const int64_t i = rem / fd, f = rem % fd;
+    T* d = dst + (c * n_dst + pos[i]) * fd + f;
+    *d = *d + src[t];
+  }
+}
+template <typename T>
+__global__ void scale_chunks_k(T* v, int64_t per_chunk, int64_t n_chunks, const double* factors,
+                               double* partials) {
+  double sq = 0.0;
+  const int64_t total = n_chunks * per_chunk;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / per_chunk;
+    T x = v[t] * (T)factors[c];     // denormalize: f32 * f32(factor) / f64 * factor
+    v[t] = x;
+    sq += (double)x * (double)x;
+  }
+  if (partials) {
+    sq = block_sum(sq);
+    if (threadIdx.x == 0) partials[blockIdx.x] = sq;
+  }
+}
+}  // namespace
+
+extern "C" int xct_gather_rows(const void* d_src, int64_t n_src, const int32_t* d_idx, int64_t m,
+                               int64_t n_chunks, int32_t fd, int f64, void* d_dst, void* stream) {
+  if (!d_src || !d_dst || (m && !d_idx)) return xct::fail(XCT_EINVAL, "gather_rows: bad argument");
+  const int64_t total = n_chunks * m * fd;
+  if (total == 0) return XCT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (f64) gather_rows_k<double><<<blocks_for(total), kThreads, 0, s>>>((const double*)d_src, n_src, d_idx, m, n_chunks, fd, (double*)d_dst);
+  else gather_rows_k<float><<<blocks_for(total), kThreads, 0, s>>>((const float*)d_src, n_src, d_idx, m, n_chunks, fd, (float*)d_dst);
+  XCT_CUDA_CHECK_LAUNCH("gather_rows");
+  return XCT_OK;
+}
+
+extern "C" int xct_accumulate_rows(void* d_dst, int64_t n_dst, const void* d_src,
+                                   const int32_t* d_pos, int64_t m, int64_t n_chunks, int32_t fd,
+                                   int f64, void* stream) {
+  if (!d_src || !d_dst || (m && !d_pos)) return xct::fail(XCT_EINVAL, "accumulate_rows: bad argument");
+  const int64_t total = n_chunks * m * fd;
+  if (total == 0) return XCT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (f64) accumulate_rows_k<double><<<blocks_for(total), kThreads, 0, s>>>((double*)d_dst, n_dst, (const double*)d_src, d_pos, m, n_chunks, fd);
+  else accumulate_rows_k<float><<<blocks_for(total), kThreads, 0, s>>>((float*)d_dst, n_dst, (const float*)d_src, d_pos, m, n_chunks, fd);
+  XCT_CUDA_CHECK_LAUNCH("accumulate_rows");
+  return XCT_OK;
+}
+
+extern "C" int xct_scale_chunks(void* d_v, int64_t per_chunk, int64_t n_chunks,
+                                const double* d_factors, int f64, double* d_scratch,
+                                double* d_sumsq, void* stream) {
+  if (!d_v || !d_factors) return xct::fail(XCT_EINVAL, "scale_chunks: bad argument");
+  const int64_t total = n_chunks * per_chunk;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (total == 0) {
+    if (d_sumsq) cudaMemsetAsync(d_sumsq, 0, sizeof(double), s);
+    return XCT_OK;
+  }
+  const int g = blocks_for(total);
+  double* partials = d_sumsq ? d_scratch : nullptr;
+  if (f64) scale_chunks_k<double><<<g, kThreads, 0, s>>>((double*)d_v, per_chunk, n_chunks, d_factors, partials);
+  else scale_chunks_k<float><<<g, kThreads, 0, s>>>((float*)d_v, per_chunk, n_chunks, d_factors, partials);
+  if (partials) final_sum_kernel<<<1, 1024, 0, s>>>(partials, g, d_sumsq);
+  XCT_CUDA_CHECK_LAUNCH("scale_chunks");
+  return XCT_OK;
+}

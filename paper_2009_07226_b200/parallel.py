@@ -14,9 +14,10 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import matrixstore, pipeline
+from . import matrixstore, pipeline  # noqa: F401
 
-__all__ = ["slice_groups", "broadcast_system", "MatrixInfo"]
+__all__ = ["slice_groups", "broadcast_system", "MatrixInfo", "DomainPartitionedSystem",
+           "NcclComm"]
 
 
 def slice_groups(num_slices: int, p_b: int) -> list:
@@ -88,3 +89,231 @@ def broadcast_system(system, config, geometry, src: int = 0):
     info = MatrixInfo(meta["num_rows"], meta["num_cols"], meta["nnz"], meta["num_angles"],
                       meta["num_detector_cols"])
     return pipeline.AssembledSystem.from_sides(info, config, geometry, fwd, adj, meta["exp"])
+
+
+# ---------------------------------------------------------------------------
+# Data-partitioned operator over GPUs (P_d = world size)
+# ---------------------------------------------------------------------------
+
+class NcclComm:
+    """Global reductions of a distributed CGLS (NCCL over NVLink)."""
+
+    def __init__(self, dev):
+        import torch
+        self.dev = dev
+        self._s = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def max_bits(self, t):
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)     # max of non-negative f64 bits
+        return t
+
+    def sum(self, x: float) -> float:
+        import torch.distributed as dist
+        self._s.fill_(x)
+        dist.all_reduce(self._s)
+        return float(self._s.item())
+
+
+class _DistSide:
+    """One direction of the partitioned operator on this rank: the local
+    staged block (rows = footprint elements) and the exchange that turns its
+    partial products into the owned outputs (K10 + NCCL p2p)."""
+
+    def __init__(self, block, fp_ids, own_ids, in_ids, fp_of, own_of, rank, dev):
+        import torch
+        self.block = block
+        self.blocks = [block]
+        self.num_inputs, self.num_outputs = len(in_ids), len(own_ids)
+        self.n_fp = len(fp_ids)
+        self.rank, self.peers = rank, len(fp_of)
+        t = lambda a: torch.as_tensor(np.asarray(a, np.int32), device=dev)
+        owner = {}
+        # positions of each peer's owned elements inside my footprint (send)
+        self.send = {}
+        for q, own_q in enumerate(own_of):
+            pos = np.nonzero(np.isin(fp_ids, own_q, assume_unique=True))[0]
+            if q == rank:
+                self.self_src = t(pos)
+                self.self_dst = t(np.searchsorted(own_ids, fp_ids[pos]))
+            elif len(pos):
+                self.send[q] = t(pos)
+        # where each peer's contributions land in my owned outputs (recv)
+        self.recv = {}
+        for s, fp_s in enumerate(fp_of):
+            if s == rank:
+                continue
+            hit = np.intersect1d(fp_s, own_ids, assume_unique=True)
+            if len(hit):
+                self.recv[s] = t(np.searchsorted(own_ids, hit))
+        del owner
+
+    def exchange_apply(self, cg, xin, out, fac) -> float:
+        """Local partial SpMM, exchange, reduction in the reference's direct
+        plan order (owner first, then senders ascending), denormalize.
+        Returns the local sum of squares of the owned outputs."""
+        import torch
+        import torch.distributed as dist
+        from . import _lib, engine
+        C, fd = cg.n_chunks, cg.f_dev
+        f64 = int(cg.out_dt == torch.float64)
+        partial = torch.empty((C, self.n_fp, fd), dtype=cg.out_dt, device=cg.dev)
+        engine.apply_side(self.block, xin, partial, row_stride=fd, chunk_stride=self.n_fp * fd,
+                          valid_cols=C * fd, ffactor_out=fd, factors=None, stream=cg.st)
+
+        def gather(idx):
+            buf = torch.empty((C, idx.numel(), fd), dtype=cg.out_dt, device=cg.dev)
+            _lib.call("xct_gather_rows", partial.data_ptr(), self.n_fp, idx.data_ptr(),
+                      idx.numel(), C, fd, f64, buf.data_ptr(), cg.st)
+            return buf
+        sends = {q: gather(idx) for q, idx in self.send.items()}
+        recvs = {s: torch.empty((C, idx.numel(), fd), dtype=cg.out_dt, device=cg.dev)
+                 for s, idx in self.recv.items()}
+        ops = [dist.P2POp(dist.isend, b, q) for q, b in sends.items()]
+        ops += [dist.P2POp(dist.irecv, b, s) for s, b in recvs.items()]
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        o = out.view(C, self.num_outputs, fd)
+        o.zero_()
+        own = gather(self.self_src)
+        _lib.call("xct_accumulate_rows", o.data_ptr(), self.num_outputs, own.data_ptr(),
+                  self.self_dst.data_ptr(), self.self_dst.numel(), C, fd, f64, cg.st)
+        for s in sorted(recvs):
+            _lib.call("xct_accumulate_rows", o.data_ptr(), self.num_outputs, recvs[s].data_ptr(),
+                      self.recv[s].data_ptr(), self.recv[s].numel(), C, fd, f64, cg.st)
+        _lib.call("xct_scale_chunks", o.data_ptr(), self.num_outputs * fd, C, fac.data_ptr(), f64,
+                  cg.scratch.data_ptr(), cg.scal.data_ptr(), cg.st)
+        return float(cg.scal[0].item())
+
+
+class DomainPartitionedSystem:
+    """Operator partitioned over the GPUs by Hilbert tile segments of both
+    planes (src/pipeline.py:104-113, src/hilbert.py:181-200): rank r owns
+    voxels T_r and rays G_r, holds A[:, T_r] (footprint rays) and
+    A[G_r, :]^T (footprint voxels), and exchanges partial sinograms /
+    tomograms with its peers over NVLink (NCCL p2p) once per application.
+    Duck-types the AssembledSystem surface used by solver.CGLSRun; the CGLS
+    vectors are distributed (each rank holds its owned elements)."""
+
+    def __init__(self, geometry, config, src: int = 0):
+        import torch
+        import torch.distributed as dist
+        from . import geometry as geo
+        from . import pipeline
+        from .pipeline import column_block, hilbert_subdomains, row_block_transposed
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.comm = NcclComm(self.device)
+        self.config, self.geometry = config, geometry
+        g = geometry
+        self.num_rows, self.num_cols = g.num_rays, g.num_voxels
+        tomo, sino = hilbert_subdomains(g, config.tile_size, self.world)
+        self.col_owned = tomo[self.rank].elements
+        self.row_owned = sino[self.rank].elements
+        self.local_cols, self.local_rows = len(self.col_owned), len(self.row_owned)
+        rw = pipeline._rows_per_warp(config)
+        schedule = config.order == "native"
+        metas = None
+        if self.rank == src:
+            A = geo.build_system_matrix(g)
+            ip, ix, v = A.host_csr32()
+            exp = (matrixstore.half_rescale_exponent(v)
+                   if config.precision in ("half", "mixed") else 0)
+            R, Cn = g.num_rays, g.num_voxels
+            n = g.grid_n
+            built = []
+            for q in range(self.world):
+                cols, rays = tomo[q].elements, sino[q].elements
+                bip, bix, bv, f_fp = column_block(ip, ix, v, R, Cn, cols)
+                t_ip, t_ix, t_v, a_fp = row_block_transposed(ip, ix, v, rays)
+                sides = []
+                for (pip, pix, pv, nr, nc, keys) in (
+                        (bip, bix, bv, len(f_fp), len(cols), (cols // n)),
+                        (t_ip, t_ix, t_v, len(a_fp), len(rays), (rays // n))):
+                    if config.order == "reference":
+                        plan = matrixstore.reference_plan(
+                            pip, pix, nr, nc, config.block_partitions,
+                            config.stage_capacity_bytes, config.ffactor, config.precision, rw,
+                            config.warps_per_cta)
+                        budget = pipeline.smem_budget_for(config, plan)
+                    else:
+                        # band keys: iz per voxel column (monotone along every
+                        # ray), view angle per ray column (ray-id order)
+                        plan = matrixstore.row_block_plan(nr, nc, rw, config.warps_per_cta,
+                                                          keys=keys.astype(np.int32))
+                        budget = config.smem_budget
+                    sides.append(matrixstore.build_format(pip, pix, pv, nr, nc, plan,
+                                                          config.precision, config.ffactor,
+                                                          exp, budget, schedule))
+                built.append((sides, f_fp, a_fp))
+            geo.clear_matrix_cache()
+            del A, ip, ix, v
+            metas = [dict(exp=exp, f_fp=b[1], a_fp=b[2]) for b in built]
+        box = [metas]
+        dist.broadcast_object_list(box, src=src, device=self.device)
+        metas = box[0]
+        self.value_scale_exp = metas[0]["exp"]
+        fp_fwd = [m["f_fp"] for m in metas]
+        fp_adj = [m["a_fp"] for m in metas]
+        # ship every rank its two formats (uploaded by the source, NCCL p2p)
+        mine = []
+        for k, (n_in, n_out) in enumerate(((len(self.col_owned), len(fp_fwd[self.rank])),
+                                           (len(self.row_owned), len(fp_adj[self.rank])))):
+            side = None
+            for q in range(self.world):
+                if self.rank == src:
+                    hf = built[q][0][k]
+                    ins = (len(tomo[q].elements), len(sino[q].elements))[k]
+                    outs = (len(fp_fwd[q]), len(fp_adj[q]))[k]
+                    blk = matrixstore.upload_format(hf, config.precision, config.ffactor, ins,
+                                                    outs, self.value_scale_exp, self.device)
+                    if q == src:
+                        side = blk
+                    else:
+                        _send_side(blk, q)
+                    del blk
+                elif q == self.rank:
+                    side = _recv_side(src, self.device)
+            mine.append(side)
+        if self.rank == src:
+            del built
+        torch.cuda.empty_cache()
+        self.forward = _DistSide(mine[0], fp_fwd[self.rank], self.row_owned, self.col_owned,
+                                 fp_fwd, [s.elements for s in sino], self.rank, self.device)
+        self.adjoint = _DistSide(mine[1], fp_adj[self.rank], self.col_owned, self.row_owned,
+                                 fp_adj, [s.elements for s in tomo], self.rank, self.device)
+
+    def gather_x(self, x_local):
+        """Assemble the full (num_cols, S) estimate on every rank (small
+        problems / tests)."""
+        import torch.distributed as dist
+        parts = [None] * self.world
+        dist.all_gather_object(parts, (self.col_owned, np.asarray(x_local)))
+        full = np.zeros((self.num_cols,) + np.asarray(x_local).shape[1:])
+        for cols, xl in parts:
+            full[cols] = xl
+        return full
+
+
+def _send_side(side, dst):
+    import torch.distributed as dist
+    dist.send_object_list([matrixstore.side_meta(side)], dst=dst,
+                          device=side.tensors["values"].device)
+    for k in sorted(side.tensors):
+        dist.send(side.tensors[k].view(-1).view(__import__("torch").uint8), dst=dst)
+
+
+def _recv_side(src, dev):
+    import torch
+    import torch.distributed as dist
+    box = [None]
+    dist.recv_object_list(box, src=src, device=dev)
+    meta = box[0]
+    tensors = {}
+    for k in sorted(meta["tensors"]):
+        shape, dtype = meta["tensors"][k]
+        t = torch.empty(shape, dtype=getattr(torch, dtype), device=dev)
+        dist.recv(t.view(-1).view(torch.uint8), src=src)
+        tensors[k] = t
+    return matrixstore.side_from_meta(meta, tensors)

@@ -126,6 +126,54 @@ def _transpose(indptr, indices, values, n_rows, n_cols):
     return t_ip, t_ix[:nnz], t_v[:nnz]
 
 
+def smem_budget_for(cfg, plan) -> int:
+    """Shared memory per CTA: the configured budget, raised for reference
+    staging so one whole reference stage fits a (double-buffered) group."""
+    if plan.kind != "reference" or cfg.stage_capacity_bytes is None:
+        return cfg.smem_budget
+    rec = matrixstore.f_dev_for(cfg.ffactor, cfg.precision) * \
+        matrixstore.element_bytes(cfg.precision)
+    cap = cfg.stage_capacity_bytes // (matrixstore.element_bytes(cfg.precision) * cfg.ffactor)
+    return max(cfg.smem_budget, min(2 * cap * rec, matrixstore.SMEM_MAX))
+
+
+def hilbert_subdomains(geometry, tile_size: int, parts: int):
+    """Tomogram and sinogram Hilbert tile segments (src/pipeline.py:104-113)."""
+    g = geometry
+    tomo = hilbert.decompose(hilbert.TileGrid("tomogram", g.grid_n, g.grid_n, tile_size), parts)
+    sino = hilbert.decompose(hilbert.TileGrid("sinogram", g.num_angles, g.num_detector_cols,
+                                              tile_size), parts)
+    return tomo, sino
+
+
+def column_block(ip, ix, v, n_rows, n_cols, cols):
+    """A[:, cols] over the rows it touches, local ids (src/matrixstore.py:130-148).
+    Returns (indptr, local col ids, values, global ids of the footprint rows)."""
+    row_of = np.repeat(np.arange(n_rows), np.diff(ip))
+    keep = np.zeros(n_cols, bool)
+    keep[cols] = True
+    sel = keep[ix]
+    rows = row_of[sel]
+    fp = np.unique(rows)
+    lr = np.searchsorted(fp, rows)
+    bip = np.concatenate(([0], np.cumsum(np.bincount(lr, minlength=len(fp))))).astype(np.int64)
+    bix = np.searchsorted(cols, ix[sel]).astype(np.int32)
+    return bip, bix, v[sel], fp
+
+
+def row_block_transposed(ip, ix, v, rows):
+    """transpose(A[rows, :]) over the columns those rows touch
+    (src/matrixstore.py:151-165, :189-201).  Returns (indptr, local row
+    positions, values, global ids of the footprint columns)."""
+    take = (np.concatenate([np.arange(ip[r], ip[r + 1]) for r in rows])
+            if len(rows) else np.empty(0, np.int64))
+    fp = np.unique(ix[take])
+    rip = np.concatenate(([0], np.cumsum(np.diff(ip)[rows]))).astype(np.int64)
+    rix = np.searchsorted(fp, ix[take]).astype(np.int32)
+    t_ip, t_ix, t_v = _transpose(rip, rix, v[take], len(rows), len(fp))
+    return t_ip, t_ix, t_v, fp
+
+
 class AssembledSystem:
     """Distributed forward/adjoint operator over one batch group's slices
     (src/pipeline.py:64-210), device resident."""
@@ -185,15 +233,7 @@ class AssembledSystem:
         return matrixstore.row_block_plan(n_rows, n_cols, rw, cfg.warps_per_cta)
 
     def _budget(self, plan) -> int:
-        """Shared memory per CTA: the configured budget, raised for reference
-        staging so one whole reference stage fits a (double-buffered) group."""
-        cfg = self.config
-        if plan.kind != "reference" or cfg.stage_capacity_bytes is None:
-            return cfg.smem_budget
-        rec = matrixstore.f_dev_for(cfg.ffactor, cfg.precision) * \
-            matrixstore.element_bytes(cfg.precision)
-        cap = cfg.stage_capacity_bytes // (matrixstore.element_bytes(cfg.precision) * cfg.ffactor)
-        return max(cfg.smem_budget, min(2 * cap * rec, matrixstore.SMEM_MAX))
+        return smem_budget_for(self.config, plan)
 
     def _single_side(self, ip, ix, v, n_rows, n_cols, kind) -> _Side:
         cfg = self.config
@@ -207,13 +247,9 @@ class AssembledSystem:
 
     def _build_partitioned(self, ip, ix, v, n_rows, n_cols):
         cfg, g = self.config, self.geometry
-        tomo = hilbert.decompose(hilbert.TileGrid("tomogram", g.grid_n, g.grid_n,
-                                                  cfg.tile_size), cfg.p_d)
-        sino = hilbert.decompose(hilbert.TileGrid("sinogram", g.num_angles,
-                                                  g.num_detector_cols, cfg.tile_size), cfg.p_d)
+        tomo, sino = hilbert_subdomains(g, cfg.tile_size, cfg.p_d)
         self.tomogram_subdomains, self.sinogram_subdomains = tomo, sino
         rw = _rows_per_warp(cfg)
-        row_of = np.repeat(np.arange(n_rows), np.diff(ip))
 
         def build(bip, bix, bv, nr, nc):
             plan = matrixstore.reference_plan(bip, bix, nr, nc, cfg.block_partitions,
@@ -223,29 +259,14 @@ class AssembledSystem:
                                                  cfg.ffactor, self.value_scale_exp,
                                                  self._budget(plan), self.device)
 
-        f_blocks, f_fp = [], []
-        for sub in tomo:         # A[:, owned cols] over the rays it touches
-            cols = sub.elements
-            keep = np.zeros(n_cols, bool)
-            keep[cols] = True
-            sel = keep[ix]
-            rows = row_of[sel]
-            fp = np.unique(rows)
-            lr = np.searchsorted(fp, rows)
-            bip = np.concatenate(([0], np.cumsum(np.bincount(lr, minlength=len(fp))))).astype(np.int64)
-            bix = np.searchsorted(cols, ix[sel]).astype(np.int32)
-            f_blocks.append(build(bip, bix, v[sel], len(fp), len(cols)))
+        f_blocks, f_fp, a_blocks, a_fp = [], [], [], []
+        for sub in tomo:
+            bip, bix, bv, fp = column_block(ip, ix, v, n_rows, n_cols, sub.elements)
+            f_blocks.append(build(bip, bix, bv, len(fp), len(sub.elements)))
             f_fp.append(fp)
-        a_blocks, a_fp = [], []
-        for sub in sino:         # transpose(A[owned rays, :]) over the voxels touched
-            rays = sub.elements
-            take = np.concatenate([np.arange(ip[r], ip[r + 1]) for r in rays]) if len(rays) else np.empty(0, np.int64)
-            cnt = np.diff(ip)[rays]
-            fp = np.unique(ix[take])
-            rip = np.concatenate(([0], np.cumsum(cnt))).astype(np.int64)
-            rix = np.searchsorted(fp, ix[take]).astype(np.int32)
-            t_ip, t_ix, t_v = _transpose(rip, rix, v[take], len(rays), len(fp))
-            a_blocks.append(build(t_ip, t_ix, t_v, len(fp), len(rays)))
+        for sub in sino:
+            t_ip, t_ix, t_v, fp = row_block_transposed(ip, ix, v, sub.elements)
+            a_blocks.append(build(t_ip, t_ix, t_v, len(fp), len(sub.elements)))
             a_fp.append(fp)
         self.forward = _Side(f_blocks, [s.elements for s in tomo], f_fp,
                              [s.elements for s in sino], n_cols, n_rows)

@@ -124,12 +124,25 @@ class _Vec:
         self.t, self.code, self.factor = t, code, factor
 
 
+class LocalComm:
+    """Reductions of a single-process solve (identity)."""
+
+    def max_bits(self, t):
+        return t
+
+    def sum(self, x: float) -> float:
+        return x
+
+
 class DeviceCG:
-    """The device state and kernels of one CGLS solve over one operator."""
+    """The device state and kernels of one CGLS solve over one operator.
+    ``comm`` supplies the global reductions when the vectors are
+    distributed over GPUs (parallel.DomainPartitionedSystem)."""
 
     def __init__(self, system, n_slices: int, precision: str):
         import torch
         self.sys = system
+        self.comm = getattr(system, "comm", None) or LocalComm()
         self.dev = system.device
         self.st = _lib.stream_handle(self.dev)
         self.prec = precision                       # vector-store policy
@@ -147,7 +160,8 @@ class DeviceCG:
         self.scal = torch.zeros(8, dtype=torch.float64, device=self.dev)
         self.bits = torch.zeros(max(self.n_chunks, 1), dtype=torch.int64, device=self.dev)
         sd = {"double": torch.float64, "single": torch.float32}.get(self.op_prec, torch.float16)
-        n_max = max(system.num_rows, system.num_cols)
+        n_max = max(getattr(system, "local_rows", system.num_rows),
+                    getattr(system, "local_cols", system.num_cols))
         self.xin_buf = torch.empty(self.n_chunks * n_max * self.f_dev, dtype=sd, device=self.dev)
         self.out_dt = torch.float64 if self.op_prec == "double" else torch.float32
         blks = [b for s in (system.forward, system.adjoint) for b in s.blocks]
@@ -166,7 +180,12 @@ class DeviceCG:
     def sum_sq_to_host(self, t, code, factor=1.0):
         _lib.call("xct_dot", t.data_ptr(), t.data_ptr(), code, t.numel(), float(factor),
                   float(factor), self.scratch.data_ptr(), self.scal.data_ptr(), self.st)
-        return float(self.scal[0].item())
+        return self.comm.sum(float(self.scal[0].item()))
+
+    def peak(self, n=1):
+        """Global max of the first n max-abs slots (IEEE bits of f64)."""
+        self.comm.max_bits(self.bits[:n])
+        return self.bits[:n].cpu().numpy().view(np.float64)
 
     def store(self, v_work, out=None) -> _Vec:
         """_VectorStore.store of a work-dtype vector (src/solver.py:97-103)."""
@@ -176,7 +195,7 @@ class DeviceCG:
         self.bits.zero_()
         _lib.call("xct_maxabs", v_work.data_ptr(), 1, v_work.numel(), 1.0, self.bits.data_ptr(),
                   self.st)
-        peak = float(self.bits[:1].cpu().numpy().view(np.float64)[0])
+        peak = float(self.peak()[0])
         factor = peak if peak > 0 else 1.0
         if out is None:
             out = torch.empty(v_work.numel(), dtype=torch.float16, device=self.dev)
@@ -200,7 +219,7 @@ class DeviceCG:
         self.bits.zero_()
         _lib.call("xct_axpy", a.t.data_ptr(), a.code, fa, b.t.data_ptr(), b.code, fb,
                   float(scale), n, None, 2, 1.0, self.bits.data_ptr(), None, None, self.st)
-        peak = float(self.bits[:1].cpu().numpy().view(np.float64)[0])
+        peak = float(self.peak()[0])
         if not math.isfinite(peak):
             return None, None, peak
         factor = peak if peak > 0 else 1.0
@@ -210,7 +229,7 @@ class DeviceCG:
                   float(scale), n, out.data_ptr(), 2, float(np.float32(factor)), None,
                   self.scratch.data_ptr(), self.scal.data_ptr() if want_sumsq else None,
                   self.st)
-        ss = float(self.scal[0].item()) if want_sumsq else None
+        ss = self.comm.sum(float(self.scal[0].item())) if want_sumsq else None
         return _Vec(out, 2, factor), ss, peak
 
     def apply(self, side, v: _Vec, out):
@@ -221,7 +240,7 @@ class DeviceCG:
         _lib.call("xct_chunk_maxabs_chunked", v.t.data_ptr(), v.code,
                   float(np.float32(v.factor)), n_in, self.n_chunks, self.f_dev,
                   self.bits.data_ptr(), self.st)
-        peaks = self.bits[:self.n_chunks].cpu().numpy().view(np.float64)
+        peaks = self.peak(self.n_chunks)
         if not np.all(np.isfinite(peaks)):
             return None, None
         factors = [float(p) if p > 0 else 1.0 for p in peaks]
@@ -230,6 +249,8 @@ class DeviceCG:
         _lib.call("xct_normalize_chunked", v.t.data_ptr(), v.code, float(np.float32(v.factor)),
                   n_in, self.n_chunks, self.f_dev, fac.data_ptr(), _lib.PREC_CODE[self.op_prec],
                   xin.data_ptr(), self.st)
+        if hasattr(side, "exchange_apply"):           # distributed (NCCL) operator
+            return factors, self.comm.sum(side.exchange_apply(self, xin, out, fac))
         if len(side.blocks) == 1 and side.input_elements[0] is None:
             blk = side.blocks[0]
             parts = self.part_buf[:self.n_chunks * blk.info.n_cta]
@@ -290,16 +311,16 @@ class CGLSRun:
         the stored residual r = store(wd(y))."""
         import torch
         cg, prec, system = self.cg, self.config.precision, self.system
-        S, n_rows, n_cols = cg.S, system.num_rows, system.num_cols
-        y = self.y
-        if isinstance(y, np.ndarray):
-            y = y.reshape(n_rows, S)
-        else:
-            y = y.reshape(n_rows, S)
+        S = cg.S
+        y = self.y.reshape(system.num_rows, S)
+        # distributed operators own a subset of the rays and voxels
+        owned = getattr(system, "row_owned", None)
+        n_rows = getattr(system, "local_rows", system.num_rows)
+        n_cols = getattr(system, "local_cols", system.num_cols)
 
         def chunk(c):
             lo, hi = c * cg.F, min(S, (c + 1) * cg.F)
-            yc = y[:, lo:hi]
+            yc = y[:, lo:hi] if owned is None else y[owned, lo:hi]
             if isinstance(yc, np.ndarray):
                 yc = torch.from_numpy(np.ascontiguousarray(yc, dtype=np.float64))
             return yc.to(device=cg.dev, dtype=torch.float64).contiguous(), hi - lo
@@ -324,14 +345,17 @@ class CGLSRun:
                       dst.data_ptr(), cg.st)
             if cg.reduced:
                 _lib.call("xct_maxabs", tmp.data_ptr(), 1, per, 1.0, rbits.data_ptr(), cg.st)
+        cg.comm.max_bits(ybits)
         if not math.isfinite(float(ybits.cpu().numpy().view(np.float64)[0])):
             raise SolverDivergence(0, prec, "measurement data contains NaN or Inf")
+        y_sq = cg.comm.sum(y_sq)
         self.y_norm = math.sqrt(y_sq)
         if self.y_norm == 0.0:
             self.done = True
             self.x = None
             return False
         if cg.reduced:
+            cg.comm.max_bits(rbits)
             peak = float(rbits.cpu().numpy().view(np.float64)[0])
             r.factor = peak if peak > 0 else 1.0
             f32 = float(np.float32(r.factor))
@@ -417,7 +441,7 @@ class CGLSRun:
     def finish(self) -> SolveResult:
         import torch
         cg, system = self.cg, self.system
-        n_cols, S = system.num_cols, cg.S
+        n_cols, S = getattr(system, "local_cols", system.num_cols), cg.S
         if self.x is None:
             out = np.zeros((n_cols, S))
             if not self.is_np:
