@@ -188,6 +188,15 @@ def run_reference_arm(args, cfg, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def _global_nnz(system):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(system.forward.block.nnz)], dtype=torch.float64,
+                     device=system.device)
+    dist.all_reduce(t)
+    return t.item()
+
+
 def metric_name(cfg):
     return (f"SpMM GFLOPS & CG s/iter ({cfg['n']}^2 x {cfg['slices']} slices/GPU, "
             f"{cfg['k']} angles, {cfg['precision']})")
@@ -199,7 +208,8 @@ def config_block(cfg, ws):
             "slices_per_gpu": cfg["slices"] if not cfg.get("strong") else -(-total // ws),
             "total_slices": total,
             "precision": cfg["precision"], "ffactor": 16, "step": "one CGLS iteration",
-            "parallelism": f"slice-batch P_b={ws}", "l2": "inputs >> L2 (matrix "
+            "parallelism": (f"image-domain P_d={ws}" if cfg.get("domain") else
+                            f"slice-batch P_b={ws}"), "l2": "inputs >> L2 (matrix "
             "streamed from HBM every application), no flush needed"}
 
 
@@ -215,6 +225,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-iters", type=int, default=None)
+    ap.add_argument("--partition", default="slices", choices=["slices", "domain"],
+                    help="multi-GPU: slice batch (P_b, default) or image-domain tiles "
+                         "with the NCCL partial-result exchange (P_d)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.precision:
@@ -235,7 +248,12 @@ def main():
     scfg = pipeline.SystemConfig(precision=cfg["precision"], ffactor=16, order=args.order)
     # slices on this rank: weak scaling = a fixed group per GPU; strong
     # scaling = the config's total split by the reference's P_b rule
-    if cfg.get("strong"):
+    domain = args.partition == "domain" and ws > 1
+    cfg["domain"] = domain
+    if domain:
+        cfg["strong"] = True          # the same problem, split by image/sinogram tiles
+        S = cfg["slices"]
+    elif cfg.get("strong"):
         lo, hi = parallel.slice_groups(cfg["slices"], ws)[rank]
         S = hi - lo
     else:
@@ -245,12 +263,21 @@ def main():
     if rank == 0:
         g, y1 = make_problem(cfg, S)
         t_matrix = time.perf_counter() - t0
-        system = pipeline.assemble(g, scfg)
+        if not domain:
+            system = pipeline.assemble(g, scfg)
         geometry.clear_matrix_cache()
         torch.cuda.empty_cache()
     else:
         g = geometry.make_geometry(cfg["k"], S, cfg["n"])
-    if ws > 1:
+    if domain:
+        import dataclasses
+        scfg = dataclasses.replace(scfg, p_d=ws)
+        system = parallel.DomainPartitionedSystem(g, scfg)
+        yt = (torch.from_numpy(y1).to(dev) if rank == 0 else
+              torch.empty((g.num_rays, 1), dtype=torch.float64, device=dev))
+        dist.broadcast(yt, src=0)
+        y1 = yt.cpu().numpy()
+    elif ws > 1:
         # one host build; the staged operator goes to every GPU over NVLink
         system = parallel.broadcast_system(system, scfg, g)
         yt = (torch.from_numpy(y1).to(dev) if rank == 0 else
@@ -260,7 +287,7 @@ def main():
     y = np.broadcast_to(y1, (g.num_rays, S))      # identical phantom slices
     torch.cuda.synchronize()
     t_assemble = time.perf_counter() - t0 - t_matrix
-    nnz = system.matrix.nnz
+    nnz = system.matrix.nnz if not domain else int(round(_global_nnz(system)))
 
     W, K = max(args.warmup, 0), max(args.steps, 1)
     run = solver.CGLSRun(system, y, solver.SolveConfig(max_iters=W + K + 1,
@@ -302,13 +329,20 @@ def main():
     b_x = matrixstore.element_bytes(cfg["precision"])
     n_chunks = -(-S // 16)
     R, C = g.num_rays, g.num_voxels
-    bytes_app = nnz * b_e * n_chunks + (R + C) * S * b_x
+
+    def side_bytes(side):       # compulsory bytes of one launch on this rank
+        blk = side.blocks[0]
+        return blk.nnz * b_e * n_chunks + (blk.n_in + blk.n_out) * S * b_x
+    bytes_fwd, bytes_adj = side_bytes(system.forward), side_bytes(system.adjoint)
+    bytes_app = (bytes_fwd + bytes_adj) / 2
     spmm_ms = [a.elapsed_time(b) for _, a, b in events]
     t_spmm = sum(spmm_ms) / 1e3
     n_spmm = len(spmm_ms)
-    achieved = bytes_app * n_spmm / t_spmm / 1e9 if t_spmm > 0 else 0.0
+    moved = sum(bytes_fwd if fw else bytes_adj for fw, _, _ in events)
+    achieved = moved / t_spmm / 1e9 if t_spmm > 0 else 0.0
     peak, peak_src = hbm_peak()
-    spmm_gflops = 2.0 * nnz * S * n_spmm / t_spmm / 1e9 if t_spmm > 0 else 0.0
+    local_nnz = (system.forward.blocks[0].nnz + system.adjoint.blocks[0].nnz) / 2
+    spmm_gflops = 2.0 * local_nnz * S * n_spmm / t_spmm / 1e9 if t_spmm > 0 else 0.0
     traffic = None
     tf = ROOT / "profiles" / f"traffic_{args.config}_{cfg['precision']}.json"
     if tf.exists():

@@ -158,8 +158,15 @@ class _DistSide:
         C, fd = cg.n_chunks, cg.f_dev
         f64 = int(cg.out_dt == torch.float64)
         partial = torch.empty((C, self.n_fp, fd), dtype=cg.out_dt, device=cg.dev)
+        ev = cg.events
+        if ev is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
         engine.apply_side(self.block, xin, partial, row_stride=fd, chunk_stride=self.n_fp * fd,
                           valid_cols=C * fd, ffactor_out=fd, factors=None, stream=cg.st)
+        if ev is not None:
+            e1.record()
+            ev.append((self is cg.sys.forward, e0, e1))
 
         def gather(idx):
             buf = torch.empty((C, idx.numel(), fd), dtype=cg.out_dt, device=cg.dev)
