@@ -291,6 +291,9 @@ class DomainPartitionedSystem:
         self.adjoint = _DistSide(mine[1], fp_adj[self.rank], self.col_owned, self.row_owned,
                                  fp_adj, [s.elements for s in tomo], self.rank, self.device)
 
+    def hbm_bytes(self) -> int:
+        return self.forward.block.hbm_bytes() + self.adjoint.block.hbm_bytes()
+
     def gather_x(self, x_local):
         """Assemble the full (num_cols, S) estimate on every rank (small
         problems / tests)."""
