@@ -269,6 +269,20 @@ def adjoint_tile_height(n: int, rows_per_warp: int, warps: int) -> int:
     return max(tx, (rw * warps) // tx * tx) // tx
 
 
+def restrict_plan(plan: Plan, row_ids: np.ndarray, col_ids: np.ndarray) -> Plan:
+    """A plan over a block of the operator (rows = global `row_ids`, local
+    columns = global `col_ids`): the global tiles restricted to the block's
+    rows (renumbered to local positions, empty tiles dropped) and the key
+    tables re-indexed by the local columns."""
+    pos = np.full(int(max(plan.cta_rows.max(), row_ids.max() if len(row_ids) else 0)) + 1, -1,
+                  np.int64)
+    pos[row_ids] = np.arange(len(row_ids))
+    rows = np.where(plan.cta_rows >= 0, pos[np.maximum(plan.cta_rows, 0)], -1)
+    keep = (rows >= 0).any(axis=1)
+    return Plan(rows[keep].astype(np.int32), plan.key_tables[:, col_ids],
+                plan.cta_table[keep], plan.rows_per_warp, plan.kind)
+
+
 def row_block_plan(n_rows: int, n_cols: int, rows_per_warp: int, warps: int,
                    keys: np.ndarray | None = None) -> Plan:
     """Consecutive rows per CTA, one key table (default: one key per column

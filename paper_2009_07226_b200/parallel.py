@@ -230,14 +230,23 @@ class DomainPartitionedSystem:
             R, Cn = g.num_rays, g.num_voxels
             n = g.grid_n
             built = []
+            if config.order != "reference":
+                # the single-GPU tiles (sinogram / voxel tiles, band keys),
+                # restricted to each rank's block
+                gf = matrixstore.assign_forward_regimes(
+                    matrixstore.forward_plan(g.num_angles, n, rw, config.warps_per_cta),
+                    g.angles, n)
+                ga = matrixstore.adjoint_plan(g.num_angles, n, rw, config.warps_per_cta)
             for q in range(self.world):
                 cols, rays = tomo[q].elements, sino[q].elements
                 bip, bix, bv, f_fp = column_block(ip, ix, v, R, Cn, cols)
                 t_ip, t_ix, t_v, a_fp = row_block_transposed(ip, ix, v, rays)
                 sides = []
-                for (pip, pix, pv, nr, nc, keys) in (
-                        (bip, bix, bv, len(f_fp), len(cols), (cols // n)),
-                        (t_ip, t_ix, t_v, len(a_fp), len(rays), (rays // n))):
+                for (pip, pix, pv, nr, nc, rows_g, cols_g, gplan) in (
+                        (bip, bix, bv, len(f_fp), len(cols), f_fp, cols,
+                         gf if config.order != "reference" else None),
+                        (t_ip, t_ix, t_v, len(a_fp), len(rays), a_fp, rays,
+                         ga if config.order != "reference" else None)):
                     if config.order == "reference":
                         plan = matrixstore.reference_plan(
                             pip, pix, nr, nc, config.block_partitions,
@@ -245,10 +254,7 @@ class DomainPartitionedSystem:
                             config.warps_per_cta)
                         budget = pipeline.smem_budget_for(config, plan)
                     else:
-                        # band keys: iz per voxel column (monotone along every
-                        # ray), view angle per ray column (ray-id order)
-                        plan = matrixstore.row_block_plan(nr, nc, rw, config.warps_per_cta,
-                                                          keys=keys.astype(np.int32))
+                        plan = matrixstore.restrict_plan(gplan, rows_g, cols_g)
                         budget = config.smem_budget
                     sides.append(matrixstore.build_format(pip, pix, pv, nr, nc, plan,
                                                           config.precision, config.ffactor,
