@@ -325,7 +325,6 @@ __global__ void __launch_bounds__(1024) spmm_staged_kernel(const Params p) {
   r2.load(p.slots, p.values, at + 2 * step, pol_e);
   r3.load(p.slots, p.values, at + 3 * step, pol_e);
   at += 4 * step;
-  int t = 0;                               // steps consumed so far (ring phase)
   // two stage buffers: group g+1 is staged while group g is consumed
   if (g0 < g1) stage_fill(p, xb, s0, g0, lp, pol_x);
   cp_async_commit();
@@ -340,28 +339,41 @@ __global__ void __launch_bounds__(1024) spmm_staged_kernel(const Params p) {
     uint32_t pb[NPL];
 #pragma unroll
     for (int qq = 0; qq < NPL; ++qq) pb[qq] = cur_buf + pbase[qq];
-    const int end = t + n4;
-    while (t < end) {
-      switch (t & 3) {
-        case 0:
-          consume<PREC, NPL>(acc, r0, pb);
-          r0.load(p.slots, p.values, at, pol_e);
-          break;
-        case 1:
-          consume<PREC, NPL>(acc, r1, pb);
-          r1.load(p.slots, p.values, at, pol_e);
-          break;
-        case 2:
-          consume<PREC, NPL>(acc, r2, pb);
-          r2.load(p.slots, p.values, at, pol_e);
-          break;
-        default:
-          consume<PREC, NPL>(acc, r3, pb);
-          r3.load(p.slots, p.values, at, pol_e);
-          break;
-      }
-      at += step;
-      ++t;
+    // full 4-step blocks, then the remainder; the ring is rotated so that
+    // the next unconsumed step is always in r0 at a group boundary
+    int k = 0;
+    for (; k + 4 <= n4; k += 4) {
+      consume<PREC, NPL>(acc, r0, pb);
+      r0.load(p.slots, p.values, at, pol_e);
+      consume<PREC, NPL>(acc, r1, pb);
+      r1.load(p.slots, p.values, at + step, pol_e);
+      consume<PREC, NPL>(acc, r2, pb);
+      r2.load(p.slots, p.values, at + 2 * step, pol_e);
+      consume<PREC, NPL>(acc, r3, pb);
+      r3.load(p.slots, p.values, at + 3 * step, pol_e);
+      at += 4 * step;
+    }
+    const int rem = n4 - k;
+    if (rem >= 1) {
+      consume<PREC, NPL>(acc, r0, pb);
+      r0.load(p.slots, p.values, at, pol_e);
+    }
+    if (rem >= 2) {
+      consume<PREC, NPL>(acc, r1, pb);
+      r1.load(p.slots, p.values, at + step, pol_e);
+    }
+    if (rem >= 3) {
+      consume<PREC, NPL>(acc, r2, pb);
+      r2.load(p.slots, p.values, at + 2 * step, pol_e);
+    }
+    at += rem * step;
+    if (rem == 1) {
+      const St tmp = r0; r0 = r1; r1 = r2; r2 = r3; r3 = tmp;
+    } else if (rem == 2) {
+      St tmp = r0; r0 = r2; r2 = tmp;
+      tmp = r1; r1 = r3; r3 = tmp;
+    } else if (rem == 3) {
+      const St tmp = r3; r3 = r2; r2 = r1; r1 = r0; r0 = tmp;
     }
   }
   cp_async_wait_all();
