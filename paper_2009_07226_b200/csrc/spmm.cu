@@ -250,30 +250,25 @@ __device__ __forceinline__ uint32_t buffer_bytes(int lp, int plane_slots) {
 constexpr int kDepth = 4;     // entry steps in flight per lane (register ring)
 constexpr int kFillUnroll = 4;
 
-// Stage the records of load group g into the buffer at shared address dst.
-// Piece-interleaved (full 32-byte sectors per pair of lanes); the map is
-// read kFillUnroll ahead so the loads are independent.
-__device__ __forceinline__ void stage_fill(const Params& p, const uint4* xb, uint32_t dst, int g,
-                                           int lp, uint64_t pol) {
-  const int64_t m0 = p.group_map_ptr[g];
-  const int pieces = (int)(p.group_map_ptr[g + 1] - m0) << lp;
+// Stage the records of load group g into the buffer at shared address dst,
+// reading the group's slot->element map from shared memory (it was copied
+// there one group earlier, so no dependent global load sits on this path).
+__device__ __forceinline__ void stage_fill(const Params& p, const uint4* xb, uint32_t dst,
+                                           const int32_t* map, int ns, int lp, uint64_t pol) {
+  const int pieces = ns << lp;
   const int NP = 1 << lp;
-  for (int i0 = threadIdx.x; i0 < pieces; i0 += blockDim.x * kFillUnroll) {
-    int32_t e[kFillUnroll];
-#pragma unroll
-    for (int u = 0; u < kFillUnroll; ++u) {
-      const int i = i0 + u * blockDim.x;
-      e[u] = i < pieces ? __ldg(p.group_map + m0 + (i >> lp)) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < kFillUnroll; ++u) {
-      const int i = i0 + u * blockDim.x;
-      if (i < pieces) {
-        const int s = i >> lp, q = i & (NP - 1);
-        cp_async16(dst + plane_base(q, lp, p.plane_slots) + ((uint32_t)s << 4),
-                   xb + ((int64_t)e[u] << lp) + q, pol);
-      }
-    }
+  for (int i = threadIdx.x; i < pieces; i += blockDim.x) {
+    const int s = i >> lp, q = i & (NP - 1);
+    cp_async16(dst + plane_base(q, lp, p.plane_slots) + ((uint32_t)s << 4),
+               xb + ((int64_t)map[s] << lp) + q, pol);
+  }
+}
+
+// Copy the slot->element map of group g into shared memory (4-byte cp.async).
+__device__ __forceinline__ void map_fill(const Params& p, int32_t* dst, int64_t m0, int ns) {
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + i);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(sa), "l"(p.group_map + m0 + i));
   }
 }
 
@@ -286,6 +281,41 @@ __device__ __forceinline__ void consume(A& acc, const St& cur, const uint32_t (&
 #pragma unroll
     for (int qq = 0; qq < NPL; ++qq) acc.fma(qq, lds128(pb[qq] + off), len);
   }
+}
+
+// One load group's slabs with the ring entered at phase P: ring slot
+// (P + i) & 3 holds the i-th next step, so no register is ever copied.
+template <int PREC, int NPL, int P, typename A, typename St>
+__device__ __forceinline__ void run_group(A& acc, St (&r)[4], int n4, int64_t& at,
+                                          const int64_t step, const uint32_t (&pb)[NPL],
+                                          const Params& p, uint64_t pol) {
+  constexpr int S0 = P, S1 = (P + 1) & 3, S2 = (P + 2) & 3, S3 = (P + 3) & 3;
+  int k = 0;
+  for (; k + 4 <= n4; k += 4) {
+    consume<PREC, NPL>(acc, r[S0], pb);
+    r[S0].load(p.slots, p.values, at, pol);
+    consume<PREC, NPL>(acc, r[S1], pb);
+    r[S1].load(p.slots, p.values, at + step, pol);
+    consume<PREC, NPL>(acc, r[S2], pb);
+    r[S2].load(p.slots, p.values, at + 2 * step, pol);
+    consume<PREC, NPL>(acc, r[S3], pb);
+    r[S3].load(p.slots, p.values, at + 3 * step, pol);
+    at += 4 * step;
+  }
+  const int rem = n4 - k;
+  if (rem >= 1) {
+    consume<PREC, NPL>(acc, r[S0], pb);
+    r[S0].load(p.slots, p.values, at, pol);
+  }
+  if (rem >= 2) {
+    consume<PREC, NPL>(acc, r[S1], pb);
+    r[S1].load(p.slots, p.values, at + step, pol);
+  }
+  if (rem >= 3) {
+    consume<PREC, NPL>(acc, r[S2], pb);
+    r[S2].load(p.slots, p.values, at + 2 * step, pol);
+  }
+  at += rem * step;
 }
 
 template <int PREC, int NPL>
@@ -319,62 +349,55 @@ __global__ void __launch_bounds__(1024) spmm_staged_kernel(const Params p) {
   const int64_t step = (int64_t)rpw * 4;
   int64_t at = (g0 < g1 ? p.slab_off[(int64_t)g0 * p.warps_per_cta + warp] : 0) +
                (int64_t)rin * 4;
-  St r0, r1, r2, r3;
-  r0.load(p.slots, p.values, at, pol_e);
-  r1.load(p.slots, p.values, at + step, pol_e);
-  r2.load(p.slots, p.values, at + 2 * step, pol_e);
-  r3.load(p.slots, p.values, at + 3 * step, pol_e);
+  St r[4];
+  r[0].load(p.slots, p.values, at, pol_e);
+  r[1].load(p.slots, p.values, at + step, pol_e);
+  r[2].load(p.slots, p.values, at + 2 * step, pol_e);
+  r[3].load(p.slots, p.values, at + 3 * step, pol_e);
   at += 4 * step;
-  // two stage buffers: group g+1 is staged while group g is consumed
-  if (g0 < g1) stage_fill(p, xb, s0, g0, lp, pol_x);
+  int phase = 0;
+  // pipeline: map(g+2) -> smem and records(g+1) -> smem while g is consumed
+  int32_t* const maps = reinterpret_cast<int32_t*>(
+      reinterpret_cast<char*>(stage) + 2 * (size_t)bb);
+  int32_t* const map0 = maps;
+  int32_t* const map1 = maps + p.plane_slots;
+  int64_t mp0 = g0 < g1 ? p.group_map_ptr[g0] : 0;
+  int64_t mp1 = g0 < g1 ? p.group_map_ptr[g0 + 1] : 0;
+  int64_t mp2 = g0 + 1 < g1 ? p.group_map_ptr[g0 + 2] : mp1;
+  if (g0 < g1) {
+    map_fill(p, map0, mp0, (int)(mp1 - mp0));
+    if (g0 + 1 < g1) map_fill(p, map1, mp1, (int)(mp2 - mp1));
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    stage_fill(p, xb, s0, map0, (int)(mp1 - mp0), lp, pol_x);
+  }
   cp_async_commit();
   for (int g = g0; g < g1; ++g) {
-    const uint32_t cur_buf = s0 + (((g - g0) & 1) ? bb : 0u);
+    const int odd = (g - g0) & 1;
+    const uint32_t cur_buf = s0 + (odd ? bb : 0u);
     const int n4 = p.slab_width[(int64_t)g * p.warps_per_cta + warp] >> 2;
+    const int64_t mp3 = g + 3 <= g1 ? p.group_map_ptr[min(g + 3, g1)] : mp2;
     cp_async_wait_all();
-    __syncthreads();                     // fill(g) visible; everyone done with g-1
-    if (g + 1 < g1) stage_fill(p, xb, s0 + (((g - g0) & 1) ? 0u : bb), g + 1, lp, pol_x);
+    __syncthreads();            // fill(g), map(g+1) visible; everyone done with g-1
+    if (g + 1 < g1)             // records of g+1 (map already in shared memory)
+      stage_fill(p, xb, s0 + (odd ? 0u : bb), odd ? map0 : map1, (int)(mp2 - mp1), lp, pol_x);
+    if (g + 2 < g1)             // map of g+2 into the buffer map(g) used
+      map_fill(p, odd ? map1 : map0, mp2, (int)(mp3 - mp2));
     cp_async_commit();
+    mp1 = mp2;
+    mp2 = mp3;
 
     uint32_t pb[NPL];
 #pragma unroll
     for (int qq = 0; qq < NPL; ++qq) pb[qq] = cur_buf + pbase[qq];
-    // full 4-step blocks, then the remainder; the ring is rotated so that
-    // the next unconsumed step is always in r0 at a group boundary
-    int k = 0;
-    for (; k + 4 <= n4; k += 4) {
-      consume<PREC, NPL>(acc, r0, pb);
-      r0.load(p.slots, p.values, at, pol_e);
-      consume<PREC, NPL>(acc, r1, pb);
-      r1.load(p.slots, p.values, at + step, pol_e);
-      consume<PREC, NPL>(acc, r2, pb);
-      r2.load(p.slots, p.values, at + 2 * step, pol_e);
-      consume<PREC, NPL>(acc, r3, pb);
-      r3.load(p.slots, p.values, at + 3 * step, pol_e);
-      at += 4 * step;
+    switch (phase) {
+      case 0: run_group<PREC, NPL, 0>(acc, r, n4, at, step, pb, p, pol_e); break;
+      case 1: run_group<PREC, NPL, 1>(acc, r, n4, at, step, pb, p, pol_e); break;
+      case 2: run_group<PREC, NPL, 2>(acc, r, n4, at, step, pb, p, pol_e); break;
+      default: run_group<PREC, NPL, 3>(acc, r, n4, at, step, pb, p, pol_e); break;
     }
-    const int rem = n4 - k;
-    if (rem >= 1) {
-      consume<PREC, NPL>(acc, r0, pb);
-      r0.load(p.slots, p.values, at, pol_e);
-    }
-    if (rem >= 2) {
-      consume<PREC, NPL>(acc, r1, pb);
-      r1.load(p.slots, p.values, at + step, pol_e);
-    }
-    if (rem >= 3) {
-      consume<PREC, NPL>(acc, r2, pb);
-      r2.load(p.slots, p.values, at + 2 * step, pol_e);
-    }
-    at += rem * step;
-    if (rem == 1) {
-      const St tmp = r0; r0 = r1; r1 = r2; r2 = r3; r3 = tmp;
-    } else if (rem == 2) {
-      St tmp = r0; r0 = r2; r2 = tmp;
-      tmp = r1; r1 = r3; r3 = tmp;
-    } else if (rem == 3) {
-      const St tmp = r3; r3 = r2; r2 = r1; r1 = r0; r0 = tmp;
-    }
+    phase = (phase + n4) & 3;
   }
   cp_async_wait_all();
 
@@ -478,7 +501,8 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   if (threads < 32 || threads > 1024) return xct::fail(XCT_EINVAL, "spmm: CTA must have 1..32 warps");
   const int64_t plane_slots = (a->max_group_slots + 7) & ~(int64_t)7;
   if (plane_slots * 16 > 65536) return xct::fail(XCT_ESTAGE, "spmm: plane offsets exceed 16 bits");
-  const int64_t need = 2 * ((plane_slots << (lp + 4)) + 128);   // double-buffered stage
+  // double-buffered stage + two slot->element maps
+  const int64_t need = 2 * ((plane_slots << (lp + 4)) + 128) + 2 * plane_slots * 4;
   if (smem_bytes < need) smem_bytes = need;
   if (smem_bytes > 227 * 1024) return xct::fail(XCT_ESTAGE, "spmm: load group exceeds shared memory");
 

@@ -586,7 +586,8 @@ def attach(side: DeviceSide) -> DeviceSide:
     side.staged = s
     plane_slots = -(-int(info.max_group_slots) // 8) * 8
     rec = side.f_dev * element_bytes(side.precision)
-    side.smem_bytes = int(2 * (plane_slots * rec + 128))
+    # two stage buffers + two slot->element maps (see spmm.cu)
+    side.smem_bytes = int(2 * (plane_slots * rec + 128) + 2 * plane_slots * 4)
     return side
 
 

@@ -50,8 +50,9 @@ class SystemConfig:
       warps_per_cta  CTA size of the staged SpMM.
       smem_budget    shared-memory bytes per CTA for one load group.
       pieces_per_lane  16-byte pieces of a staged record each lane owns (1, 2
-                     or 4; lanes per row = record pieces / this; None = up
-                     to 4: one lane per row for FP16/FP32 at F=16).
+                     or 4; lanes per row = record pieces / this; None = 2,
+                     measured fastest with the 64-register K6 at F=16: one
+                     lane per row in FP16, two in FP32).
       build          "streamed": never materialize the whole matrix -- the
                      projection format is built per chunk of views, the back
                      projection per band of voxels, from Siddon regenerated
@@ -104,7 +105,7 @@ class _Side:
 
 
 def _rows_per_warp(cfg) -> int:
-    ppl = cfg.pieces_per_lane or 4
+    ppl = cfg.pieces_per_lane or 2
     return 32 // matrixstore.lanes_for(cfg.ffactor, cfg.precision, ppl)
 
 
