@@ -318,6 +318,22 @@ class CGLSRun:
         n_rows = getattr(system, "local_rows", system.num_rows)
         n_cols = getattr(system, "local_cols", system.num_cols)
 
+        # host measurements that fit comfortably are uploaded once, whole
+        # rows at a time (contiguous, pinned-speed copies); larger ones are
+        # streamed one slice chunk at a time
+        is_host = isinstance(y, np.ndarray) or not y.is_cuda
+        nbytes = n_rows * S * 8
+        if is_host and nbytes <= min(16 << 30, torch.cuda.mem_get_info(cg.dev)[0] // 4):
+            yd = torch.empty((n_rows, S), dtype=torch.float64, device=cg.dev)
+            rows_per = max(1, (256 << 20) // max(1, S * 8))
+            for r0 in range(0, n_rows, rows_per):
+                r1 = min(n_rows, r0 + rows_per)
+                blk = y[r0:r1] if owned is None else y[owned[r0:r1]]
+                if isinstance(blk, np.ndarray):
+                    blk = torch.from_numpy(np.ascontiguousarray(blk, dtype=np.float64))
+                yd[r0:r1].copy_(blk, non_blocking=True)
+            y, owned = yd, None
+
         def chunk(c):
             lo, hi = c * cg.F, min(S, (c + 1) * cg.F)
             yc = y[:, lo:hi] if owned is None else y[owned, lo:hi]
@@ -366,7 +382,7 @@ class CGLSRun:
                 _lib.call("xct_axpy", tmp.data_ptr(), 1, 1.0, None, 1, 1.0, 0.0, per,
                           r.t[c * per:(c + 1) * per].data_ptr(), 2, f32, None,
                           cg.scratch.data_ptr(), None, cg.st)
-        del tmp
+        del tmp, y
         self.r = r
         if cg.reduced:
             self.x = _Vec(torch.zeros(cg.numel(n_cols), dtype=torch.float16, device=cg.dev), 2, 1.0)
