@@ -69,6 +69,16 @@ int xct_csr_filter_cols(const int64_t* d_indptr, const int32_t* d_indices,
                         int32_t col_hi, int64_t* d_counts, const int64_t* d_out_ptr,
                         int32_t* d_out_idx, double* d_out_val, void* stream);
 
+/* Row/column-mapped restriction (per-rank blocks of the data-partitioned
+ * operator, built streamed; cf. src/matrixstore.py:130-165): entry j of row
+ * r is kept when d_row_keep[r] != 0 (or d_row_keep == NULL) and
+ * d_col_map[col] >= 0, and its column becomes d_col_map[col].  Count pass
+ * when d_counts != NULL, else fill pass; order preserved. */
+int xct_csr_filter_map(const int64_t* d_indptr, const int32_t* d_indices,
+                       const double* d_values, int64_t n_rows, const uint8_t* d_row_keep,
+                       const int32_t* d_col_map, int64_t* d_counts, const int64_t* d_out_ptr,
+                       int32_t* d_out_idx, double* d_out_val, void* stream);
+
 /* ---------------------------------------------------------------------------
  * K5  staged execution format (host builder)
  * replaces matrixstore.build_staged / pack (src/matrixstore.py:250-262,

@@ -50,6 +50,7 @@ _SIGS = {
     "xct_siddon_count": (i32, [vp, vp, i32, i32, i32, i32, f64, vp, vp]),
     "xct_siddon_fill": (i32, [vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp]),
     "xct_csr_filter_cols": (i32, [vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp]),
+    "xct_csr_filter_map": (i32, [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]),
     "xct_format_build": (i32, [i64, i64, vp, vp, vp, i64, i64, i64, vp, vp, vp, i64, i32,
                                i32, i32, i32, i32, C.POINTER(vp)]),
     "xct_format_get_info": (i32, [vp, C.POINTER(FormatInfo)]),
@@ -121,7 +122,7 @@ KERNELS_PER_CALL = {"xct_dot": 2, "xct_sum_f64": 1, "xct_spmm": 1, "xct_maxabs":
                     "xct_chunk_maxabs": 1, "xct_normalize": 1, "xct_chunk_maxabs_chunked": 1,
                     "xct_normalize_chunked": 1, "xct_unchunk_f64": 1, "xct_chunk_from_f64": 1,
                     "xct_csr_spmm_f64": 1, "xct_siddon_count": 1, "xct_siddon_fill": 1,
-                    "xct_csr_filter_cols": 1, "xct_gather_rows": 1,
+                    "xct_csr_filter_cols": 1, "xct_csr_filter_map": 1, "xct_gather_rows": 1,
                     "xct_accumulate_rows": 1, "xct_scale_chunks": 2}
 launch_count = [0]
 

@@ -238,3 +238,67 @@ extern "C" int xct_csr_filter_cols(const int64_t* d_indptr, const int32_t* d_ind
   XCT_CUDA_CHECK_LAUNCH("csr_filter_cols");
   return XCT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Row/column-mapped restriction of a device CSR (per-rank blocks of the
+// data-partitioned operator, built streamed: src/matrixstore.py:130-165).
+// Keeps entry j of row r when row_keep[r] (or row_keep == NULL) and
+// col_map[col] >= 0; the kept column is rewritten to col_map[col].
+namespace {
+__global__ void csr_map_count_kernel(const int64_t* __restrict__ indptr,
+                                     const int32_t* __restrict__ indices, int64_t n_rows,
+                                     const uint8_t* __restrict__ row_keep,
+                                     const int32_t* __restrict__ col_map,
+                                     int64_t* __restrict__ counts) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = 0;
+    if (!row_keep || row_keep[r])
+      for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) c += col_map[indices[j]] >= 0;
+    counts[r] = c;
+  }
+}
+__global__ void csr_map_fill_kernel(const int64_t* __restrict__ indptr,
+                                    const int32_t* __restrict__ indices,
+                                    const double* __restrict__ values, int64_t n_rows,
+                                    const uint8_t* __restrict__ row_keep,
+                                    const int32_t* __restrict__ col_map,
+                                    const int64_t* __restrict__ out_ptr,
+                                    int32_t* __restrict__ out_idx, double* __restrict__ out_val) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (row_keep && !row_keep[r]) continue;
+    int64_t o = out_ptr[r];
+    for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) {
+      const int32_t m = col_map[indices[j]];
+      if (m >= 0) {
+        out_idx[o] = m;
+        out_val[o] = values[j];
+        ++o;
+      }
+    }
+  }
+}
+}  // namespace
+
+extern "C" int xct_csr_filter_map(const int64_t* d_indptr, const int32_t* d_indices,
+                                  const double* d_values, int64_t n_rows,
+                                  const uint8_t* d_row_keep, const int32_t* d_col_map,
+                                  int64_t* d_counts, const int64_t* d_out_ptr,
+                                  int32_t* d_out_idx, double* d_out_val, void* stream) {
+  if (!d_indptr || !d_col_map || n_rows < 0) return xct::fail(XCT_EINVAL, "csr_filter_map: bad argument");
+  if (n_rows == 0) return XCT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d_counts) {
+    csr_map_count_kernel<<<grid_for(n_rows, 128), 128, 0, s>>>(d_indptr, d_indices, n_rows,
+                                                              d_row_keep, d_col_map, d_counts);
+  } else {
+    if (!d_out_ptr || !d_out_idx || !d_out_val)
+      return xct::fail(XCT_EINVAL, "csr_filter_map: fill pass needs output arrays");
+    csr_map_fill_kernel<<<grid_for(n_rows, 128), 128, 0, s>>>(
+        d_indptr, d_indices, d_values, n_rows, d_row_keep, d_col_map, d_out_ptr, d_out_idx,
+        d_out_val);
+  }
+  XCT_CUDA_CHECK_LAUNCH("csr_filter_map");
+  return XCT_OK;
+}

@@ -222,6 +222,11 @@ class DomainPartitionedSystem:
         rw = pipeline._rows_per_warp(config)
         schedule = config.order == "native"
         metas = None
+        if config.order != "reference" and (
+                config.build == "streamed" or
+                (config.build == "auto" and 1.2 * g.num_angles * g.grid_n ** 2 > 4e9)):
+            self._init_streamed(g, config, tomo, sino)
+            return
         if self.rank == src:
             A = geo.build_system_matrix(g)
             ip, ix, v = A.host_csr32()
@@ -297,6 +302,30 @@ class DomainPartitionedSystem:
         self.adjoint = _DistSide(mine[1], fp_adj[self.rank], self.col_owned, self.row_owned,
                                  fp_adj, [s.elements for s in tomo], self.rank, self.device)
 
+    def _init_streamed(self, g, config, tomo, sino):
+        """Every rank builds its own blocks (no whole matrix anywhere)."""
+        import os
+        import torch
+        import torch.distributed as dist
+        fparts, f_fp, aparts, a_fp, exp = build_rank_blocks_streamed(
+            g, config, tomo, sino, self.rank, self.device)
+        self.value_scale_exp = exp
+        box = [None] * self.world
+        dist.all_gather_object(box, (f_fp, a_fp))
+        fp_fwd = [b[0] for b in box]
+        fp_adj = [b[1] for b in box]
+        fwd = matrixstore.upload_format(fparts, config.precision, config.ffactor,
+                                        len(self.col_owned), len(f_fp), exp, self.device)
+        adj = matrixstore.upload_format(aparts, config.precision, config.ffactor,
+                                        len(self.row_owned), len(a_fp), exp, self.device)
+        del fparts, aparts
+        torch.cuda.empty_cache()
+        self.forward = _DistSide(fwd, f_fp, self.row_owned, self.col_owned, fp_fwd,
+                                 [s.elements for s in sino], self.rank, self.device)
+        self.adjoint = _DistSide(adj, a_fp, self.col_owned, self.row_owned, fp_adj,
+                                 [s.elements for s in tomo], self.rank, self.device)
+        dist.barrier()
+
     def hbm_bytes(self) -> int:
         return self.forward.block.hbm_bytes() + self.adjoint.block.hbm_bytes()
 
@@ -333,3 +362,111 @@ def _recv_side(src, dev):
         dist.recv(t.view(-1).view(torch.uint8), src=src)
         tensors[k] = t
     return matrixstore.side_from_meta(meta, tensors)
+
+
+def _filter_map(ip, ix, v, rows, row_keep, col_map, st, dev):
+    """Device CSR restriction (xct_csr_filter_map) -> host (counts, idx, val)."""
+    import torch
+    from . import _lib
+    cnt = torch.empty(rows, dtype=torch.int64, device=dev)
+    rk = row_keep.data_ptr() if row_keep is not None else None
+    _lib.call("xct_csr_filter_map", ip.data_ptr(), ix.data_ptr(), v.data_ptr(), rows, rk,
+              col_map.data_ptr(), cnt.data_ptr(), None, None, None, st)
+    optr = torch.zeros(rows + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(cnt, 0, out=optr[1:])
+    m = int(optr[-1])
+    oi = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    ov = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+    _lib.call("xct_csr_filter_map", ip.data_ptr(), ix.data_ptr(), v.data_ptr(), rows, rk,
+              col_map.data_ptr(), None, optr.data_ptr(), oi.data_ptr(), ov.data_ptr(), st)
+    return cnt.cpu().numpy(), oi[:m].cpu().numpy(), ov[:m].cpu().numpy()
+
+
+def build_rank_blocks_streamed(g, config, tomo, sino, rank, dev, n_threads=None):
+    """This rank's forward block A[:, T_r] and back-projection block
+    A[G_r, :]^T built without the whole matrix: Siddon regenerated per view
+    chunk on this GPU, restricted on the device (xct_csr_filter_map), staged
+    per chunk / voxel band on the host.  Every rank builds its own blocks in
+    parallel.  Returns (fwd parts, fwd footprint rays, adj parts, adj
+    footprint voxels, value_scale_exp)."""
+    import torch
+    from . import _lib, pipeline
+    sa = pipeline.StreamedAssembly(g, config)
+    rw = sa.rw
+    n, R, Cn = g.grid_n, g.num_rays, g.num_voxels
+    st = _lib.stream_handle(dev)
+    ta = matrixstore.forward_tile_height(n, rw, config.warps_per_cta)
+    chunks = sa._chunks(ta)
+    exp = sa._exponent(chunks) if config.precision in ("half", "mixed") else 0
+    schedule = config.order == "native"
+    cols, rays = tomo[rank].elements, sino[rank].elements
+    # forward: columns -> local owned index, rows = rays touching them
+    cmap = np.full(Cn, -1, np.int32)
+    cmap[cols] = np.arange(len(cols), dtype=np.int32)
+    d_cmap = torch.from_numpy(cmap).to(dev)
+    fparts, fps = [], []
+    base = 0
+    for k0, k1 in chunks:
+        ip, ix, v = sa._siddon(k0, k1)
+        rows = (k1 - k0) * n
+        cnt, bix, bv = _filter_map(ip, ix, v, rows, None, d_cmap, st, dev)
+        keep = np.nonzero(cnt)[0]
+        fp = (k0 * n + keep).astype(np.int64)
+        if len(fp) == 0:
+            continue
+        bip = np.concatenate(([0], np.cumsum(cnt[keep]))).astype(np.int64)
+        gplan = matrixstore.assign_forward_regimes(
+            matrixstore.forward_plan(g.num_angles, n, rw, config.warps_per_cta, k0, k1),
+            g.angles, n)
+        plan = matrixstore.restrict_plan(gplan, fp, cols)
+        hf = matrixstore.build_format(bip, bix, bv, len(fp), len(cols), plan, config.precision,
+                                      config.ffactor, exp, config.smem_budget, schedule)
+        hf.cta_rows = np.where(hf.cta_rows >= 0, hf.cta_rows + base, -1).astype(np.int32)
+        fparts.append(hf)
+        fps.append(fp)
+        base += len(fp)
+    f_fp = np.concatenate(fps) if fps else np.empty(0, np.int64)
+    # back projection: owned rays x voxel bands, transposed per band
+    rkeep = np.zeros(R, np.uint8)
+    rkeep[rays] = 1
+    d_rkeep = torch.from_numpy(rkeep).to(dev)
+    tz = matrixstore.adjoint_tile_height(n, rw, config.warps_per_cta)
+    per = max(1, int(sa.BAND_NNZ // (1.2 * g.num_angles * n)))
+    per = max(tz, per // tz * tz)
+    aparts, aps = [], []
+    base = 0
+    for z0 in range(0, n, per):
+        z1 = min(n, z0 + per)
+        lo, hi = z0 * n, z1 * n
+        bmap = np.full(Cn, -1, np.int32)
+        bmap[lo:hi] = np.arange(hi - lo, dtype=np.int32)
+        d_bmap = torch.from_numpy(bmap).to(dev)
+        counts, idx, val = [], [], []
+        for k0, k1 in chunks:
+            ip, ix, v = sa._siddon(k0, k1)
+            rows = (k1 - k0) * n
+            cnt, bix, bv = _filter_map(ip, ix, v, rows, d_rkeep[k0 * n:k1 * n], d_bmap, st, dev)
+            keep_rows = rkeep[k0 * n:k1 * n].astype(bool)
+            counts.append(cnt[keep_rows])            # owned rays, ascending
+            idx.append(bix)
+            val.append(bv)
+        bip = np.zeros(len(rays) + 1, np.int64)
+        np.cumsum(np.concatenate(counts), out=bip[1:])
+        bix, bv = np.concatenate(idx), np.concatenate(val)
+        t_ip, t_ix, t_v = pipeline._transpose(bip, bix, bv, len(rays), hi - lo)
+        nz = np.nonzero(np.diff(t_ip))[0]                   # band voxels touched
+        if len(nz) == 0:
+            continue
+        vp = (lo + nz).astype(np.int64)
+        sub_ip = np.concatenate((t_ip[nz], t_ip[-1:])).astype(np.int64)   # drop empty rows
+        gplan = matrixstore.adjoint_plan(g.num_angles, n, rw, config.warps_per_cta, z0, z1)
+        plan = matrixstore.restrict_plan(gplan, vp, rays)
+        hf = matrixstore.build_format(sub_ip, t_ix, t_v, len(vp), len(rays), plan,
+                                      config.precision, config.ffactor, exp,
+                                      config.smem_budget, schedule)
+        hf.cta_rows = np.where(hf.cta_rows >= 0, hf.cta_rows + base, -1).astype(np.int32)
+        aparts.append(hf)
+        aps.append(vp)
+        base += len(vp)
+    a_fp = np.concatenate(aps) if aps else np.empty(0, np.int64)
+    return fparts, f_fp, aparts, a_fp, exp
