@@ -511,26 +511,49 @@ extern "C" int xct_csr_transpose(int64_t n_rows, int64_t n_cols, const int64_t* 
                                  const int32_t* indices, const double* values,
                                  int64_t* t_indptr, int32_t* t_indices, double* t_values,
                                  int n_threads) {
-  (void)n_threads;
   if (!indptr || !t_indptr) return xct::fail(XCT_EINVAL, "csr_transpose: null argument");
-  const int64_t nnz = indptr[n_rows] - indptr[0];
-  std::vector<int64_t> next(n_cols + 1, 0);
-  for (int64_t j = indptr[0]; j < indptr[n_rows]; ++j) {
-    int32_t c = indices[j];
-    if (c < 0 || c >= n_cols) return xct::fail(XCT_EINVAL, "csr_transpose: column out of range");
-    ++next[c + 1];
-  }
-  for (int64_t c = 0; c < n_cols; ++c) next[c + 1] += next[c];
-  std::memcpy(t_indptr, next.data(), (n_cols + 1) * 8);
-  (void)nnz;
-  // rows visited in ascending order: entries of each column end up sorted by
-  // row id and, for repeated (row, col) pairs, in CSR order (stable)
-  for (int64_t r = 0; r < n_rows; ++r) {
-    for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) {
-      int64_t at = next[indices[j]]++;
-      t_indices[at] = (int32_t)r;
-      t_values[at] = values[j];
+  // Parallel stable counting transpose: rows are split into T contiguous
+  // blocks; block t's entries of column c go after those of blocks < t, and
+  // inside a block rows are visited in order, so every column lists its rows
+  // ascending (and repeated (row, col) pairs in CSR order) -- exactly the
+  // stable argsort of src/matrixstore.py:189-201.
+  int T = n_threads < 1 ? 1 : n_threads;
+  if ((int64_t)T * n_cols > (int64_t)1 << 31) T = std::max<int64_t>(1, ((int64_t)1 << 31) / std::max<int64_t>(n_cols, 1));
+  if (T > n_rows) T = (int)std::max<int64_t>(1, n_rows);
+  std::vector<int64_t> rb(T + 1);
+  for (int t = 0; t <= T; ++t) rb[t] = n_rows * t / T;
+  std::vector<int32_t> cnt((size_t)T * n_cols, 0);
+  std::atomic<int> bad{0};
+  parallel_for(T, T, [&](int64_t t) {
+    int32_t* c = cnt.data() + (size_t)t * n_cols;
+    for (int64_t j = indptr[rb[t]]; j < indptr[rb[t + 1]]; ++j) {
+      const int32_t col = indices[j];
+      if (col < 0 || col >= n_cols) { bad = 1; return; }
+      ++c[col];
     }
+  });
+  if (bad) return xct::fail(XCT_EINVAL, "csr_transpose: column out of range");
+  // column totals -> t_indptr; per-block starting offsets in place
+  t_indptr[0] = 0;
+  for (int64_t c = 0; c < n_cols; ++c) {
+    int64_t run = t_indptr[c];
+    for (int t = 0; t < T; ++t) {
+      int32_t& x = cnt[(size_t)t * n_cols + c];
+      const int64_t k = x;
+      x = (int32_t)(run - t_indptr[c]);      // offset inside column c
+      run += k;
+    }
+    t_indptr[c + 1] = run;
   }
+  parallel_for(T, T, [&](int64_t t) {
+    int32_t* c = cnt.data() + (size_t)t * n_cols;
+    for (int64_t r = rb[t]; r < rb[t + 1]; ++r)
+      for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) {
+        const int32_t col = indices[j];
+        const int64_t at = t_indptr[col] + c[col]++;
+        t_indices[at] = (int32_t)r;
+        t_values[at] = values[j];
+      }
+  });
   return XCT_OK;
 }

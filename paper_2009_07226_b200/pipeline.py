@@ -420,6 +420,25 @@ def assemble_from_matrix(matrix, config: SystemConfig | None = None) -> Assemble
     return AssembledSystem(matrix, config, geometry=None)
 
 
+def _log(msg):
+    import os
+    import sys
+    if os.environ.get("XCT_VERBOSE"):
+        print(f"[xct] {msg}", file=sys.stderr, flush=True)
+
+
+class _Timer:
+    def __init__(self):
+        import time
+        self.t, self.acc = time.perf_counter(), {}
+
+    def lap(self, key):
+        import time
+        now = time.perf_counter()
+        self.acc[key] = self.acc.get(key, 0.0) + now - self.t
+        self.t = now
+
+
 class StreamedAssembly:
     """Operator build that never holds the whole matrix (needed at 2048^2 x
     2048 views, 1.03e10 entries): Siddon is regenerated on the device per
@@ -483,21 +502,28 @@ class StreamedAssembly:
         n = g.grid_n
         ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta)
         parts = []
+        tm = _Timer()
         for k0, k1 in self._chunks(ta):
             plan = matrixstore.forward_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, k0, k1)
             plan = matrixstore.assign_forward_regimes(plan, g.angles, n)
             base = k0 * n
             plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - base, -1).astype(np.int32)
+            tm.lap("plan")
             ip, ix, v = self._siddon(k0, k1)
             ip, ix, v = ip.cpu().numpy(), ix.cpu().numpy(), v.cpu().numpy()
+            tm.lap("siddon+d2h")
             hf = matrixstore.build_format(ip, ix, v, (k1 - k0) * n, g.num_voxels, plan,
                                           cfg.precision, cfg.ffactor, exp, cfg.smem_budget,
                                           schedule=cfg.order == "native")
+            tm.lap("format")
             hf.cta_rows = np.where(hf.cta_rows >= 0, hf.cta_rows + base, -1).astype(np.int32)
             parts.append(hf)
             self.nnz += int(hf.info["nnz"])
-        return matrixstore.upload_format(parts, cfg.precision, cfg.ffactor, g.num_voxels,
+        side = matrixstore.upload_format(parts, cfg.precision, cfg.ffactor, g.num_voxels,
                                          g.num_rays, exp, self.dev)
+        tm.lap("upload")
+        _log(f"forward build {tm.acc}")
+        return side
 
     def _adjoint(self, exp, chunks):
         import torch
@@ -508,6 +534,7 @@ class StreamedAssembly:
         per = max(tz, per // tz * tz)
         st = _lib.stream_handle(self.dev)
         parts = []
+        tm = _Timer()
         for z0 in range(0, n, per):
             z1 = min(n, z0 + per)
             lo, hi = z0 * n, z1 * n
@@ -528,21 +555,29 @@ class StreamedAssembly:
                 counts.append(cnt.cpu().numpy())
                 idx.append(oi[:m].cpu().numpy())
                 val.append(ov[:m].cpu().numpy())
+            tm.lap("siddon+filter+d2h")
             bip = np.zeros(R + 1, np.int64)
             np.cumsum(np.concatenate(counts), out=bip[1:])
             bix, bv = np.concatenate(idx), np.concatenate(val)
             del counts, idx, val
+            tm.lap("concat")
             t_ip, t_ix, t_v = _transpose(bip, bix, bv, R, hi - lo)
             del bip, bix, bv
+            tm.lap("transpose")
             plan = matrixstore.adjoint_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, z0, z1)
             plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - lo, -1).astype(np.int32)
+            tm.lap("plan")
             hf = matrixstore.build_format(t_ip, t_ix, t_v, hi - lo, R, plan, cfg.precision,
                                           cfg.ffactor, exp, cfg.smem_budget,
                                           schedule=cfg.order == "native")
+            tm.lap("format")
             hf.cta_rows = np.where(hf.cta_rows >= 0, hf.cta_rows + lo, -1).astype(np.int32)
             parts.append(hf)
-        return matrixstore.upload_format(parts, cfg.precision, cfg.ffactor, R, g.num_voxels,
+        side = matrixstore.upload_format(parts, cfg.precision, cfg.ffactor, R, g.num_voxels,
                                          exp, self.dev)
+        tm.lap("upload")
+        _log(f"adjoint build {tm.acc}")
+        return side
 
     def run(self) -> AssembledSystem:
         import torch
