@@ -155,3 +155,75 @@ def stream_handle(device=None) -> int:
 
 def n_threads() -> int:
     return max(1, min(64, os.cpu_count() or 1))
+
+
+_STAGE_BYTES = 1 << 26
+_stage = {}
+
+
+def _staging(device):
+    """Two reusable pinned host buffers (plus their copy-done events)."""
+    import torch
+    key = str(device)
+    if key not in _stage:
+        bufs = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        _stage[key] = (bufs, [b.numpy() for b in bufs],
+                       [torch.cuda.Event() for _ in range(2)])
+    return _stage[key]
+
+
+def to_host(t) -> np.ndarray:
+    """Device tensor -> new numpy array, via double-buffered pinned staging
+    (pageable ``.cpu()`` runs at a few GB/s; the matrix builds move tens of
+    GB this way)."""
+    import torch
+    t = t.contiguous()
+    out = np.empty(tuple(t.shape), dtype=torch.empty((), dtype=t.dtype).numpy().dtype)
+    n = t.numel() * t.element_size()
+    if n == 0:
+        return out
+    if t.device.type != "cuda":
+        out[...] = t.numpy()
+        return out
+    src = t.reshape(-1).view(torch.uint8)
+    dst = out.reshape(-1).view(np.uint8)
+    bufs, views, evs = _staging(t.device)
+    blocks = [(b, min(n, b + _STAGE_BYTES)) for b in range(0, n, _STAGE_BYTES)]
+    for i, (b0, b1) in enumerate(blocks):
+        bufs[i & 1][:b1 - b0].copy_(src[b0:b1], non_blocking=True)
+        evs[i & 1].record()
+        if i:
+            p0, p1 = blocks[i - 1]
+            evs[(i - 1) & 1].synchronize()
+            dst[p0:p1] = views[(i - 1) & 1][:p1 - p0]
+    p0, p1 = blocks[-1]
+    evs[(len(blocks) - 1) & 1].synchronize()
+    dst[p0:p1] = views[(len(blocks) - 1) & 1][:p1 - p0]
+    return out
+
+
+def to_device(a: np.ndarray, dst) -> None:
+    """numpy array -> the contiguous device tensor ``dst`` (same byte size),
+    via double-buffered pinned staging."""
+    import torch
+    a = np.ascontiguousarray(a)
+    n = a.nbytes
+    if n == 0:
+        return
+    if dst.numel() * dst.element_size() != n or not dst.is_contiguous():
+        raise ValueError("to_device: size mismatch")
+    src = a.reshape(-1).view(np.uint8)
+    d = dst.reshape(-1).view(torch.uint8)
+    if dst.device.type != "cuda":        # host-side (gloo) format copies
+        d.copy_(torch.from_numpy(src))
+        return
+    bufs, views, evs = _staging(dst.device)
+    for i, b0 in enumerate(range(0, n, _STAGE_BYTES)):
+        b1 = min(n, b0 + _STAGE_BYTES)
+        if i >= 2:
+            evs[i & 1].synchronize()     # the copy that last used this buffer
+        views[i & 1][:b1 - b0] = src[b0:b1]
+        d[b0:b1].copy_(bufs[i & 1][:b1 - b0], non_blocking=True)
+        evs[i & 1].record()
+    for e in evs:
+        e.synchronize()

@@ -369,22 +369,44 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
       }
     double wmax = 0.0;
     int64_t nunder = 0;
-    // entries of every (group, thread-row) in (key, CSR position) order
+    // entries of every (group, thread-row) in (key, CSR position) order, in
+    // one flat buffer: a row's key-sorted entries visit the groups in order,
+    // so (group, row) lists are contiguous spans
     struct Ent { int32_t slot; int64_t j; };
-    std::vector<std::vector<Ent>> per(ng * rows_per_cta);
+    struct Span { const Ent* p; int64_t n; size_t size() const { return (size_t)n; }
+                  const Ent& operator[](size_t i) const { return p[i]; } };
+    std::vector<Ent> flat;
+    std::vector<int64_t> gofs((size_t)(ng + 1) * rows_per_cta, 0);
+    flat.reserve(1024);
     for (int64_t t = 0; t < rows_per_cta; ++t) {
       int32_t r = cta_rows[b * rows_per_cta + t];
-      if (r < 0) continue;
-      ent.clear();
-      for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) ent.push_back({keys[indices[j]], j});
-      std::stable_sort(ent.begin(), ent.end(),
-                       [](const std::pair<int32_t, int64_t>& a,
-                          const std::pair<int32_t, int64_t>& c) { return a.first < c.first; });
-      for (auto& e : ent) {
-        const int32_t col = indices[e.second];
-        per[(int64_t)group_of[col] * rows_per_cta + t].push_back({slot_of[col], e.second});
+      const int64_t row0 = (int64_t)flat.size();
+      if (r >= 0) {
+        ent.clear();
+        bool sorted = true;
+        for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) {
+          const int32_t k = keys[indices[j]];
+          if (!ent.empty() && k < ent.back().first) sorted = false;
+          ent.push_back({k, j});
+        }
+        if (!sorted)
+          std::stable_sort(ent.begin(), ent.end(),
+                           [](const std::pair<int32_t, int64_t>& a,
+                              const std::pair<int32_t, int64_t>& c) { return a.first < c.first; });
+        for (auto& e : ent) flat.push_back({slot_of[indices[e.second]], e.second});
+      }
+      // gofs[t*(ng+1)+g] = start of group g's span inside the flat buffer
+      int64_t at = row0;
+      const int64_t end = (int64_t)flat.size();
+      for (int64_t g = 0; g <= ng; ++g) {
+        while (g < ng && at < end && group_of[indices[flat[at].j]] < g) ++at;
+        gofs[(size_t)t * (ng + 1) + g] = g < ng ? at : end;
       }
     }
+    auto per_span = [&](int64_t g, int64_t t) {
+      const int64_t a = gofs[(size_t)t * (ng + 1) + g], e = gofs[(size_t)t * (ng + 1) + g + 1];
+      return Span{flat.data() + a, e - a};
+    };
     auto write = [&](int64_t gg, int64_t w, int64_t rin, int64_t n, int32_t slot, int64_t j) {
       int64_t at = F->slab_off[gg * warps + w] + ((n >> 2) * rows_per_warp + rin) * 4 + (n & 3);
       F->slots[at] = (uint16_t)slot;
@@ -418,7 +440,7 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
         const int64_t width = F->slab_width[gg * warps + w];
         if (!bank.on()) {
           for (int64_t rin = 0; rin < rows_per_warp; ++rin) {
-            const auto& L = per[g * rows_per_cta + w * rows_per_warp + rin];
+            const Span L = per_span(g, w * rows_per_warp + rin);
             for (size_t n = 0; n < L.size(); ++n) write(gg, w, rin, (int64_t)n, L[n].slot, L[n].j);
           }
           continue;
@@ -428,7 +450,7 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
           step_slot.assign(width, -1);
           std::vector<std::pair<int64_t, int32_t>> owner;   // edge -> (rin, list index)
           for (int64_t rr = 0; rr < bank.rq; ++rr) {
-            const auto& L = per[g * rows_per_cta + w * rows_per_warp + q0 + rr];
+            const Span L = per_span(g, w * rows_per_warp + q0 + rr);
             for (size_t n = 0; n < L.size(); ++n) {
               if (!colorer.add((int)rr, bank.cls(L[n].slot))) {
                 std::lock_guard<std::mutex> lk(err_mu);
@@ -442,7 +464,7 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
           std::vector<char> used((size_t)bank.rq * width, 0);
           for (size_t e = 0; e < owner.size(); ++e) {
             const int64_t rin = owner[e].first;
-            const Ent& E = per[g * rows_per_cta + w * rows_per_warp + rin][owner[e].second];
+            const Ent& E = per_span(g, w * rows_per_warp + rin)[owner[e].second];
             const int64_t n = colorer.col[e];
             write(gg, w, rin, n, E.slot, E.j);
             used[(size_t)(rin - q0) * width + n] = 1;

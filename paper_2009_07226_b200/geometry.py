@@ -159,6 +159,7 @@ class SystemMatrix:
         self.d_indptr, self.d_indices, self.d_values = d_indptr, d_indices, d_values
         self._nnz = int(d_indices.numel())
         self._host = None
+        self._host32 = None
 
     def release_device(self) -> None:
         """Drop the device CSR (keeps host copies if already materialized)."""
@@ -177,11 +178,21 @@ class SystemMatrix:
                    np.asarray(values, np.float64))
         return m
 
+    def _h32(self):
+        """(indptr i64, indices i32, values f64) host copies, fetched once."""
+        if getattr(self, "_host32", None) is None:
+            if self._host is not None:
+                ip, ix, v = self._host
+                self._host32 = (ip, ix.astype(np.int32), v)
+            else:
+                self._host32 = (_lib.to_host(self.d_indptr), _lib.to_host(self.d_indices),
+                                _lib.to_host(self.d_values))
+        return self._host32
+
     def _h(self):
         if self._host is None:
-            self._host = (self.d_indptr.cpu().numpy(),
-                          self.d_indices.cpu().numpy().astype(np.int64),
-                          self.d_values.cpu().numpy())
+            ip, ix, v = self._h32()
+            self._host = (ip, ix.astype(np.int64), v)
         return self._host
 
     @property
@@ -202,8 +213,7 @@ class SystemMatrix:
 
     def host_csr32(self):
         """(indptr i64, indices i32, values f64) host arrays for the builders."""
-        ip, _, v = self._h()
-        return ip, self.d_indices.cpu().numpy(), v
+        return self._h32()
 
     def row(self, r: int) -> RaySegmentList:
         s, e = self.indptr[r], self.indptr[r + 1]

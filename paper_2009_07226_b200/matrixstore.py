@@ -524,10 +524,10 @@ def upload_format(hf, precision: str, ffactor: int, n_in: int, n_out: int,
 
     def put(name, at, arr):
         if len(arr):
-            T[name][at:at + len(arr)].copy_(torch.from_numpy(np.ascontiguousarray(arr)))
+            _lib.to_device(arr, T[name][at:at + len(arr)])
 
     c_off = g_off = s_off = e_off = r_off = 0
-    block = 1 << 26
+    block = 1 << 25
     for p in parts:
         a, inf = p.arrays, p.info
         put("cta_group_ptr", c_off, a["cta_group_ptr"][:-1] + g_off)
@@ -538,13 +538,19 @@ def upload_format(hf, precision: str, ffactor: int, n_in: int, n_out: int,
         put("cta_rows", r_off, p.cta_rows)
         n = int(inf["n_padded"])
         for b0 in range(0, n, block):
+            # records are packed on the device: offset = slot*16, and for
+            # half/mixed word = offset<<16 | fp16 bits
             b1 = min(n, b0 + block)
-            off = a["slots"][b0:b1].astype(np.uint32) << 4
+            ds = torch.empty(b1 - b0, dtype=torch.int16, device=dev)
+            _lib.to_device(a["slots"][b0:b1].view(np.int16), ds)
+            off = (ds.to(torch.int64) & 0xFFFF) << 4
             if packed:
-                word = (off << 16) | a["values"][b0:b1].view(np.uint16)
-                put("values", e_off + b0, word.view(np.int32))
+                dv = torch.empty(b1 - b0, dtype=torch.int16, device=dev)
+                _lib.to_device(a["values"][b0:b1].view(np.int16), dv)
+                word = (off << 16) | (dv.to(torch.int64) & 0xFFFF)
+                T["values"][e_off + b0:e_off + b1].copy_(word.view(torch.int32)[0::2])
             else:
-                put("slots", e_off + b0, off.astype(np.uint16).view(np.int16))
+                T["slots"][e_off + b0:e_off + b1].copy_(off.view(torch.int16)[0::4])
                 put("values", e_off + b0, a["values"][b0:b1])
         c_off += int(inf["n_cta"])
         g_off += int(inf["n_groups"])

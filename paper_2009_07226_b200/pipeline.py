@@ -510,7 +510,7 @@ class StreamedAssembly:
             plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - base, -1).astype(np.int32)
             tm.lap("plan")
             ip, ix, v = self._siddon(k0, k1)
-            ip, ix, v = ip.cpu().numpy(), ix.cpu().numpy(), v.cpu().numpy()
+            ip, ix, v = _lib.to_host(ip), _lib.to_host(ix), _lib.to_host(v)
             tm.lap("siddon+d2h")
             hf = matrixstore.build_format(ip, ix, v, (k1 - k0) * n, g.num_voxels, plan,
                                           cfg.precision, cfg.ffactor, exp, cfg.smem_budget,
@@ -552,9 +552,9 @@ class StreamedAssembly:
                 ov = torch.empty(max(m, 1), dtype=torch.float64, device=self.dev)
                 _lib.call("xct_csr_filter_cols", ip.data_ptr(), ix.data_ptr(), v.data_ptr(),
                           rows, lo, hi, None, optr.data_ptr(), oi.data_ptr(), ov.data_ptr(), st)
-                counts.append(cnt.cpu().numpy())
-                idx.append(oi[:m].cpu().numpy())
-                val.append(ov[:m].cpu().numpy())
+                counts.append(_lib.to_host(cnt))
+                idx.append(_lib.to_host(oi[:m]))
+                val.append(_lib.to_host(ov[:m]))
             tm.lap("siddon+filter+d2h")
             bip = np.zeros(R + 1, np.int64)
             np.cumsum(np.concatenate(counts), out=bip[1:])
