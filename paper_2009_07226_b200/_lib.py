@@ -172,18 +172,21 @@ def _staging(device):
     return _stage[key]
 
 
-def to_host(t) -> np.ndarray:
-    """Device tensor -> new numpy array, via double-buffered pinned staging
-    (pageable ``.cpu()`` runs at a few GB/s; the matrix builds move tens of
-    GB this way)."""
+def to_host(t, out: np.ndarray | None = None) -> np.ndarray:
+    """Device tensor -> numpy array (new, or the contiguous ``out`` of the
+    same byte size), via double-buffered pinned staging (pageable ``.cpu()``
+    runs at a few GB/s; the matrix builds move tens of GB this way)."""
     import torch
     t = t.contiguous()
-    out = np.empty(tuple(t.shape), dtype=torch.empty((), dtype=t.dtype).numpy().dtype)
+    if out is None:
+        out = np.empty(tuple(t.shape), dtype=torch.empty((), dtype=t.dtype).numpy().dtype)
+    elif out.nbytes != t.numel() * t.element_size() or not out.flags.c_contiguous:
+        raise ValueError("to_host: out does not match")
     n = t.numel() * t.element_size()
     if n == 0:
         return out
     if t.device.type != "cuda":
-        out[...] = t.numpy()
+        out.reshape(-1).view(np.uint8)[:] = t.reshape(-1).view(torch.uint8).numpy()
         return out
     src = t.reshape(-1).view(torch.uint8)
     dst = out.reshape(-1).view(np.uint8)

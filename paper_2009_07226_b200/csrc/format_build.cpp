@@ -18,8 +18,12 @@
 // load and the warp's loads are contiguous.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -164,8 +168,11 @@ struct xct_format {
   std::vector<int32_t> group_map;
   std::vector<int64_t> slab_off;
   std::vector<int32_t> slab_width;
-  std::vector<uint16_t> slots;
-  std::vector<uint8_t> values;
+  // slabs: uninitialised allocations, zeroed CTA by CTA in phase C
+  std::unique_ptr<uint16_t[]> slots;
+  std::unique_ptr<uint8_t[]> values;
+  int64_t n_padded = 0;
+  int vbytes = 0;
 };
 
 namespace {
@@ -186,6 +193,18 @@ void parallel_for(int64_t n, int n_threads, F fn) {
   worker();
   for (auto& th : pool) th.join();
 }
+
+struct PhaseLog {
+  bool on = std::getenv("XCT_VERBOSE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[xct] format_build %s %.3f s\n", what,
+                 std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
 
 }  // namespace
 
@@ -216,6 +235,7 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
       return xct::fail(XCT_EINVAL, "format_build: schedule lanes do not match rows_per_warp");
     bank.init(sched_log2_pieces, sched_log2_lanes);
   }
+  PhaseLog plog;
   std::vector<CtaPlan> plans(n_cta);
   std::mutex err_mu;
   int err = XCT_OK;
@@ -225,16 +245,24 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
   parallel_for(n_cta, n_threads, [&](int64_t b) {
     CtaPlan& P = plans[b];
     const int32_t* keys = key_tables + (int64_t)cta_table[b] * n_cols;
+    // distinct columns first (a per-thread stamp per column), then sort
+    // only the footprint
+    static thread_local std::vector<int64_t> stamp;
+    static std::atomic<int64_t> stamp_gen{0};
+    if ((int64_t)stamp.size() < n_cols) stamp.assign(n_cols, -1);
+    const int64_t mark = stamp_gen.fetch_add(1);
     std::vector<KC> all;
     for (int64_t t = 0; t < rows_per_cta; ++t) {
       int32_t r = cta_rows[b * rows_per_cta + t];
       if (r < 0) continue;
-      for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) all.push_back({keys[indices[j]], indices[j]});
+      for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) {
+        const int32_t col = indices[j];
+        if (stamp[col] == mark) continue;
+        stamp[col] = mark;
+        all.push_back({keys[col], col});
+      }
     }
     std::sort(all.begin(), all.end(), kc_less);
-    all.erase(std::unique(all.begin(), all.end(),
-                          [](const KC& a, const KC& c) { return a.key == c.key && a.col == c.col; }),
-              all.end());
     P.foot.swap(all);
     // whole keys per group, at most `capacity` elements per group
     int64_t cur = 0, i = 0, n = (int64_t)P.foot.size();
@@ -297,6 +325,7 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
     }
   });
   if (err) return xct::fail(err, err_msg);
+  plog.lap("A");
 
   // ---- phase B: global offsets ---------------------------------------------
   xct_format* F = new (std::nothrow) xct_format();
@@ -318,13 +347,16 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
     F->group_map.assign(n_slots, 0);
     F->slab_off.assign(n_groups * warps, 0);
     F->slab_width.assign(n_groups * warps, 0);
-    F->slots.assign(n_padded, 0);
-    F->values.assign(n_padded * vbytes, 0);
+    F->slots.reset(new uint16_t[std::max<int64_t>(n_padded, 1)]);
+    F->values.reset(new uint8_t[std::max<int64_t>(n_padded, 1) * vbytes]);
+    F->n_padded = n_padded;
+    F->vbytes = vbytes;
   } catch (...) {
     delete F;
     return xct::fail(XCT_ENOMEM, "format_build: out of host memory");
   }
-  std::vector<int64_t> cta_slot0(n_cta + 1, 0);
+  plog.lap("B-alloc");
+  std::vector<int64_t> cta_slot0(n_cta + 1, 0), cta_e0(n_cta + 1, 0);
   {
     // a warp's slabs of all groups of its tile are contiguous ([tile][warp]
     // [group]): the kernel streams them as one strided sequence, prefetching
@@ -332,6 +364,7 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
     int64_t gi = 0, so = 0, eo = 0;
     for (int64_t b = 0; b < n_cta; ++b) {
       cta_slot0[b] = so;
+      cta_e0[b] = eo;
       const CtaPlan& P = plans[b];
       int64_t ng = P.gstart.empty() ? 0 : (int64_t)P.gstart.size() - 1;
       for (int64_t g = 0; g < ng; ++g) {
@@ -346,8 +379,10 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
         }
       gi += ng;
     }
+    cta_e0[n_cta] = eo;
   }
 
+  plog.lap("B");
   // ---- phase C: fill maps and slabs ----------------------------------------
   const double scale = std::ldexp(1.0, value_scale_exp);
   std::vector<double> worst(n_cta, 0.0);
@@ -357,6 +392,9 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
     const CtaPlan& P = plans[b];
     const int32_t* keys = key_tables + (int64_t)cta_table[b] * n_cols;
     const int64_t g0 = F->cta_group_ptr[b];
+    std::memset(F->slots.get() + cta_e0[b], 0, (size_t)(cta_e0[b + 1] - cta_e0[b]) * 2);
+    std::memset(F->values.get() + cta_e0[b] * vbytes, 0,
+                (size_t)(cta_e0[b + 1] - cta_e0[b]) * vbytes);
     for (size_t i = 0; i < P.foot.size(); ++i) F->group_map[cta_slot0[b] + i] = P.foot[i].col;
     const int64_t ng = P.gstart.empty() ? 0 : (int64_t)P.gstart.size() - 1;
     std::vector<std::pair<int32_t, int64_t>> ent;   // (key, csr position)
@@ -413,7 +451,7 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
       if (j < 0) return;                       // padding: value stays 0
       double v = values[j] * scale;           // exact power-of-two rescale
       double back;
-      uint8_t* dst = F->values.data() + at * vbytes;
+      uint8_t* dst = F->values.get() + at * vbytes;
       if (precision == XCT_DOUBLE) {
         std::memcpy(dst, &v, 8);
         back = v;
@@ -487,6 +525,7 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
     return xct::fail(err, err_msg);
   }
 
+  plog.lap("C");
   F->info.n_cta = n_cta;
   F->info.rows_per_cta = rows_per_cta;
   F->info.rows_per_warp = rows_per_warp;
@@ -522,8 +561,19 @@ extern "C" int xct_format_export(const xct_format* f, int32_t* cta_group_ptr,
   cp(group_map, f->group_map.data(), f->group_map.size() * 4);
   cp(slab_off, f->slab_off.data(), f->slab_off.size() * 8);
   cp(slab_width, f->slab_width.data(), f->slab_width.size() * 4);
-  cp(slots, f->slots.data(), f->slots.size() * 2);
-  cp(values, f->values.data(), f->values.size());
+  // the slabs are GBs: copy them in parallel blocks
+  const int T = (int)std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  auto pcp = [&](void* dst, const void* src, size_t n) {
+    if (!dst || !n) return;
+    const size_t blk = std::max<size_t>(1 << 22, (n + T - 1) / T);
+    const int64_t nb = (int64_t)((n + blk - 1) / blk);
+    parallel_for(nb, T, [&](int64_t i) {
+      const size_t a = (size_t)i * blk, e = std::min(n, a + blk);
+      std::memcpy((uint8_t*)dst + a, (const uint8_t*)src + a, e - a);
+    });
+  };
+  pcp(slots, f->slots.get(), (size_t)f->n_padded * 2);
+  pcp(values, f->values.get(), (size_t)f->n_padded * f->vbytes);
   return XCT_OK;
 }
 

@@ -116,11 +116,12 @@ def _csr_host(matrix):
             np.asarray(matrix.values, np.float64))
 
 
-def _transpose(indptr, indices, values, n_rows, n_cols):
+def _transpose(indptr, indices, values, n_rows, n_cols, alloc=None):
     nnz = len(indices)
+    alloc = alloc or (lambda name, n, dt: np.empty(n, dt))
     t_ip = np.empty(n_cols + 1, np.int64)
-    t_ix = np.empty(max(nnz, 1), np.int32)
-    t_v = np.empty(max(nnz, 1), np.float64)
+    t_ix = alloc("t_ix", max(nnz, 1), np.int32)
+    t_v = alloc("t_v", max(nnz, 1), np.float64)
     _lib.call("xct_csr_transpose", n_rows, n_cols, indptr.ctypes.data,
               indices.ctypes.data if nnz else None, values.ctypes.data if nnz else None,
               t_ip.ctypes.data, t_ix.ctypes.data, t_v.ctypes.data, _lib.n_threads())
@@ -454,6 +455,27 @@ class StreamedAssembly:
         self.g, self.cfg = geometry, config
         self.dev = device()
         self.rw = _rows_per_warp(config)
+        self._pool = {}
+
+    def _buf(self, name, n, dtype, pinned=False):
+        """Reusable host buffer (page-locked for the D2H targets): fresh
+        allocations per chunk would pay the page faults again every time."""
+        import torch
+        dt = np.dtype(dtype)
+        need = int(n) * dt.itemsize
+        t = self._pool.get(name)
+        if t is None or t.numel() < need:
+            self._pool.pop(name, None)
+            t = torch.empty(int(need * 1.05) + 64, dtype=torch.uint8, pin_memory=pinned)
+            self._pool[name] = t
+        return t[:need].numpy().view(dt)
+
+    def _d2h(self, name, t):
+        """Device tensor -> pooled host array (through the pinned staging;
+        page-locking GBs up front costs more than it saves)."""
+        import torch
+        out = self._buf(name, t.numel(), torch.empty((), dtype=t.dtype).numpy().dtype)
+        return _lib.to_host(t, out=out)
 
     def _chunks(self, align: int):
         g = self.g
@@ -510,7 +532,7 @@ class StreamedAssembly:
             plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - base, -1).astype(np.int32)
             tm.lap("plan")
             ip, ix, v = self._siddon(k0, k1)
-            ip, ix, v = _lib.to_host(ip), _lib.to_host(ix), _lib.to_host(v)
+            ip, ix, v = self._d2h("f_ip", ip), self._d2h("f_ix", ix), self._d2h("f_v", v)
             tm.lap("siddon+d2h")
             hf = matrixstore.build_format(ip, ix, v, (k1 - k0) * n, g.num_voxels, plan,
                                           cfg.precision, cfg.ffactor, exp, cfg.smem_budget,
@@ -538,7 +560,12 @@ class StreamedAssembly:
         for z0 in range(0, n, per):
             z1 = min(n, z0 + per)
             lo, hi = z0 * n, z1 * n
-            counts, idx, val = [], [], []
+            # the band's entries go straight from the pinned staging into
+            # one host CSR (capacity from the ~1.27 rays/view/voxel of a
+            # parallel beam; grown if ever short)
+            counts = []
+            cap = int((hi - lo) * g.num_angles * 1.45) + 1024
+            bix, bv, at = self._buf("a_ix", cap, np.int32), self._buf("a_v", cap, np.float64), 0
             for k0, k1 in chunks:
                 ip, ix, v = self._siddon(k0, k1)
                 rows = (k1 - k0) * n
@@ -552,16 +579,23 @@ class StreamedAssembly:
                 ov = torch.empty(max(m, 1), dtype=torch.float64, device=self.dev)
                 _lib.call("xct_csr_filter_cols", ip.data_ptr(), ix.data_ptr(), v.data_ptr(),
                           rows, lo, hi, None, optr.data_ptr(), oi.data_ptr(), ov.data_ptr(), st)
+                if at + m > cap:
+                    cap = max(at + m, int(cap * 1.5))
+                    bix, bv = bix[:at].copy(), bv[:at].copy()
+                    bix2, bv2 = self._buf("a_ix", cap, np.int32), self._buf("a_v", cap, np.float64)
+                    bix2[:at], bv2[:at] = bix, bv
+                    bix, bv = bix2, bv2
                 counts.append(_lib.to_host(cnt))
-                idx.append(_lib.to_host(oi[:m]))
-                val.append(_lib.to_host(ov[:m]))
+                _lib.to_host(oi[:m], out=bix[at:at + m])
+                _lib.to_host(ov[:m], out=bv[at:at + m])
+                at += m
             tm.lap("siddon+filter+d2h")
             bip = np.zeros(R + 1, np.int64)
             np.cumsum(np.concatenate(counts), out=bip[1:])
-            bix, bv = np.concatenate(idx), np.concatenate(val)
-            del counts, idx, val
+            bix, bv = bix[:at], bv[:at]
+            del counts
             tm.lap("concat")
-            t_ip, t_ix, t_v = _transpose(bip, bix, bv, R, hi - lo)
+            t_ip, t_ix, t_v = _transpose(bip, bix, bv, R, hi - lo, alloc=self._buf)
             del bip, bix, bv
             tm.lap("transpose")
             plan = matrixstore.adjoint_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, z0, z1)
@@ -588,10 +622,12 @@ class StreamedAssembly:
         exp = self._exponent(chunks) if cfg.precision in ("half", "mixed") else 0
         self.nnz = 0
         fwd = self._forward(exp)
+        self._pool.clear()
         import gc
         gc.collect()
         torch.cuda.empty_cache()
         adj = self._adjoint(exp, chunks)
+        self._pool.clear()
         torch.cuda.empty_cache()
         info = MatrixInfo(g.num_rays, g.num_voxels, self.nnz, g.num_angles, g.num_detector_cols)
         return AssembledSystem.from_sides(info, cfg, g, fwd, adj, exp)
