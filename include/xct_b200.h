@@ -157,6 +157,11 @@ typedef struct {
   const uint16_t* d_slots;          /* [n_padded]                        */
   const void* d_values;             /* [n_padded] storage dtype          */
   int64_t max_group_slots;
+  int32_t contract;    /* single only: FFMA (one rounding) instead of the
+                          reference's multiply-then-add; native order only */
+  int32_t chunk_group; /* F-chunks of a tile launched adjacently (their CTAs
+                          share the tile's entry stream through L2); the
+                          largest power of two <= this dividing n_chunks */
 } xct_staged;
 
 typedef struct {

@@ -35,7 +35,8 @@ class Staged(C.Structure):
                 ("rows_per_warp", i64), ("n_groups", i64),
                 ("d_cta_rows", vp), ("d_cta_group_ptr", vp), ("d_group_map_ptr", vp),
                 ("d_group_map", vp), ("d_slab_off", vp), ("d_slab_width", vp),
-                ("d_slots", vp), ("d_values", vp), ("max_group_slots", i64)]
+                ("d_slots", vp), ("d_values", vp), ("max_group_slots", i64),
+                ("contract", i32), ("chunk_group", i32)]
 
 
 class Epilogue(C.Structure):

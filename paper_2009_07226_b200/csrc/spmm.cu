@@ -43,6 +43,8 @@ struct Params {
   int64_t n_in;
   int32_t rows_per_cta, warps_per_cta, log2_lanes, log2_pieces, n_cta;
   int32_t plane_slots;      // slots per shared-memory plane (multiple of 8)
+  int32_t chunk_group;      // F-chunks of one tile scheduled back to back
+  int32_t n_chunks;
   // epilogue
   void* out;
   int64_t row_stride, chunk_stride;
@@ -157,7 +159,7 @@ template <> struct Step<XCT_DOUBLE> {
 
 // ---- per-precision accumulators over NPL 16-byte pieces -----------------------
 
-template <int PREC, int NPL> struct Acc;
+template <int PREC, int NPL, bool CONTRACT = false> struct Acc;
 
 template <int NPL> struct Acc<XCT_MIXED, NPL> {   // fp16 storage, fp32 accumulate
   static constexpr int V = 8;                      // slices per 16-byte piece
@@ -203,7 +205,9 @@ template <int NPL> struct Acc<XCT_HALF, NPL> {     // fp16 storage and accumulat
   }
 };
 
-template <int NPL> struct Acc<XCT_SINGLE, NPL> {   // fp32 storage and accumulate
+// CONTRACT (native order only): one FFMA per slice instead of the
+// reference's multiply-then-add -- a single rounding, half the FP issue.
+template <int NPL, bool CONTRACT> struct Acc<XCT_SINGLE, NPL, CONTRACT> {
   static constexpr int V = 4;
   float a[4 * NPL];
   __device__ void zero() {
@@ -213,8 +217,12 @@ template <int NPL> struct Acc<XCT_SINGLE, NPL> {   // fp32 storage and accumulat
   __device__ void fma(int q, const uint4& r, float len) {
     const unsigned w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      a[4 * q + i] = __fadd_rn(a[4 * q + i], __fmul_rn(__uint_as_float(w[i]), len));
+    for (int i = 0; i < 4; ++i) {
+      if constexpr (CONTRACT)
+        a[4 * q + i] = __fmaf_rn(__uint_as_float(w[i]), len, a[4 * q + i]);
+      else
+        a[4 * q + i] = __fadd_rn(a[4 * q + i], __fmul_rn(__uint_as_float(w[i]), len));
+    }
   }
   __device__ float out(int i, float scale) const { return a[i] * scale; }
 };
@@ -318,14 +326,19 @@ __device__ __forceinline__ void run_group(A& acc, St (&r)[4], int n4, int64_t& a
   at += rem * step;
 }
 
-template <int PREC, int NPL>
+template <int PREC, int NPL, bool CONTRACT>
 __global__ void __launch_bounds__(1024) spmm_staged_kernel(const Params p) {
-  using A = Acc<PREC, NPL>;
+  using A = Acc<PREC, NPL, CONTRACT>;
   using St = Step<PREC>;
   constexpr int V = A::V;
   extern __shared__ uint4 stage[];
-  const int b = blockIdx.x;
-  const int chunk = blockIdx.y;
+  // CTA id -> (tile, chunk): the chunk_group F-chunks of a tile are adjacent
+  // in launch order, so they run concurrently and share the tile's entry
+  // stream through L2 (one HBM read per chunk group instead of per chunk).
+  const int64_t id = blockIdx.x;
+  const int G = p.chunk_group;
+  const int b = (int)((id / G) % p.n_cta);
+  const int chunk = (int)(id / ((int64_t)G * p.n_cta)) * G + (int)(id % G);
   const int lg = p.log2_lanes;               // lanes per row = 1 << lg
   const int lp = p.log2_pieces;              // 16-byte pieces per record = 1 << lp
   const int rpw = 32 >> lg;
@@ -446,29 +459,30 @@ __global__ void __launch_bounds__(1024) spmm_staged_kernel(const Params p) {
   }
 }
 
-template <int PREC, int NPL>
+template <int PREC, int NPL, bool CONTRACT>
 int launch(const Params& p, int64_t n_chunks, int threads, int64_t smem, cudaStream_t s) {
   static int configured = -1;
   if (configured < (int)smem) {
-    cudaError_t e = cudaFuncSetAttribute(spmm_staged_kernel<PREC, NPL>,
+    cudaError_t e = cudaFuncSetAttribute(spmm_staged_kernel<PREC, NPL, CONTRACT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
       return xct::fail(XCT_ECUDA, std::string("spmm smem attribute: ") + cudaGetErrorString(e));
     configured = (int)smem;
   }
-  dim3 grid((unsigned)p.n_cta, (unsigned)n_chunks);
-  spmm_staged_kernel<PREC, NPL><<<grid, threads, smem, s>>>(p);
+  const int64_t n_blocks = (int64_t)p.n_cta * n_chunks;
+  if (n_blocks > 0x7fffffffLL) return xct::fail(XCT_EINVAL, "spmm: grid too large");
+  spmm_staged_kernel<PREC, NPL, CONTRACT><<<(unsigned)n_blocks, threads, smem, s>>>(p);
   XCT_CUDA_CHECK_LAUNCH("spmm_staged");
   return XCT_OK;
 }
 
-template <int PREC>
+template <int PREC, bool CONTRACT = false>
 int launch_npl(const Params& p, int npl, int64_t n_chunks, int threads, int64_t smem,
                cudaStream_t s) {
   switch (npl) {
-    case 1: return launch<PREC, 1>(p, n_chunks, threads, smem, s);
-    case 2: return launch<PREC, 2>(p, n_chunks, threads, smem, s);
-    case 4: return launch<PREC, 4>(p, n_chunks, threads, smem, s);
+    case 1: return launch<PREC, 1, CONTRACT>(p, n_chunks, threads, smem, s);
+    case 2: return launch<PREC, 2, CONTRACT>(p, n_chunks, threads, smem, s);
+    case 4: return launch<PREC, 4, CONTRACT>(p, n_chunks, threads, smem, s);
     default: return xct::fail(XCT_EINVAL, "spmm: pieces per lane must be 1, 2 or 4");
   }
 }
@@ -497,6 +511,11 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   const int npl = 1 << (lp - lg);
   if (a->n_cta == 0 || n_chunks == 0) return XCT_OK;
   if (n_chunks > 65535) return xct::fail(XCT_EINVAL, "spmm: too many chunks for one launch");
+  if (a->contract && precision != XCT_SINGLE)
+    return xct::fail(XCT_EINVAL, "spmm: contract applies to single precision only");
+  // largest power of two <= chunk_group that divides n_chunks
+  int G = 1;
+  while (G * 2 <= a->chunk_group && n_chunks % (G * 2) == 0) G *= 2;
   const int threads = (int)(a->warps_per_cta * 32);
   if (threads < 32 || threads > 1024) return xct::fail(XCT_EINVAL, "spmm: CTA must have 1..32 warps");
   const int64_t plane_slots = (a->max_group_slots + 7) & ~(int64_t)7;
@@ -523,6 +542,8 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   p.log2_pieces = lp;
   p.n_cta = (int32_t)a->n_cta;
   p.plane_slots = (int32_t)plane_slots;
+  p.chunk_group = G;
+  p.n_chunks = (int32_t)n_chunks;
   p.out = ep->d_out;
   p.row_stride = ep->row_stride;
   p.chunk_stride = ep->chunk_stride;
@@ -534,7 +555,9 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   cudaStream_t s = (cudaStream_t)stream;
   switch (precision) {
     case XCT_DOUBLE: return launch_npl<XCT_DOUBLE>(p, npl, n_chunks, threads, smem_bytes, s);
-    case XCT_SINGLE: return launch_npl<XCT_SINGLE>(p, npl, n_chunks, threads, smem_bytes, s);
+    case XCT_SINGLE:
+      return a->contract ? launch_npl<XCT_SINGLE, true>(p, npl, n_chunks, threads, smem_bytes, s)
+                         : launch_npl<XCT_SINGLE>(p, npl, n_chunks, threads, smem_bytes, s);
     case XCT_HALF: return launch_npl<XCT_HALF>(p, npl, n_chunks, threads, smem_bytes, s);
     default: return launch_npl<XCT_MIXED>(p, npl, n_chunks, threads, smem_bytes, s);
   }

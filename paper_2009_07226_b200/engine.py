@@ -9,6 +9,7 @@ projection of the pipeline and of CGLS goes through it.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -58,6 +59,10 @@ class PartialResult:
         return self.values.shape[1]
 
 
+# tuning override of the chunk-group schedule (tools/spmm_probe.py sweeps)
+_TUNE_GROUP = int(os.environ["XCT_SPMM_CHUNK_GROUP"]) if os.environ.get("XCT_SPMM_CHUNK_GROUP") else None
+
+
 def apply_side(side: DeviceSide, x_chunked, out, *, row_stride: int, chunk_stride: int,
                valid_cols: int, ffactor_out: int, factors=None, dot_partials=None,
                stream=None) -> None:
@@ -80,6 +85,8 @@ def apply_side(side: DeviceSide, x_chunked, out, *, row_stride: int, chunk_strid
     ep.d_factors = None if factors is None else factors.data_ptr()
     ep.d_dot_partials = None if dot_partials is None else dot_partials.data_ptr()
     st = stream if stream is not None else _lib.stream_handle(x_chunked.device)
+    if _TUNE_GROUP is not None:
+        side.staged.chunk_group = _TUNE_GROUP
     _lib.check(_lib.lib().xct_spmm(C.byref(side.staged), _lib.PREC_CODE[side.precision],
                                    x_chunked.data_ptr(), side.n_in, n_chunks, side.f_dev,
                                    C.byref(ep), side.smem_bytes, st), "xct_spmm")

@@ -358,6 +358,8 @@ class DeviceSide:
     staged: _lib.Staged = field(repr=False, default=None)
     smem_bytes: int = 0
     plan_kind: str = ""
+    contract: bool = False       # single: FFMA instead of multiply-then-add
+    chunk_group: int = 1         # F-chunks of a tile launched adjacently
 
     @property
     def nnz(self) -> int:
@@ -589,6 +591,8 @@ def attach(side: DeviceSide) -> DeviceSide:
     s.d_slab_width = t["slab_width"].data_ptr()
     s.d_slots = t["slots"].data_ptr()
     s.d_values = t["values"].data_ptr()
+    s.contract = int(bool(side.contract) and side.precision == "single")
+    s.chunk_group = max(1, int(side.chunk_group))
     side.staged = s
     plane_slots = -(-int(info.max_group_slots) // 8) * 8
     rec = side.f_dev * element_bytes(side.precision)
@@ -597,11 +601,24 @@ def attach(side: DeviceSide) -> DeviceSide:
     return side
 
 
+def set_execution(side: DeviceSide, contract: bool, chunk_group: int) -> DeviceSide:
+    """Kernel execution knobs of a built side (no rebuild): FFMA
+    contraction (single precision, native order only) and the number of
+    F-chunks of a tile launched back to back."""
+    side.contract = bool(contract) and side.precision == "single"
+    side.chunk_group = max(1, int(chunk_group))
+    if side.staged is not None:
+        side.staged.contract = int(side.contract)
+        side.staged.chunk_group = side.chunk_group
+    return side
+
+
 def side_meta(side: DeviceSide) -> dict:
     """Picklable description of a side (everything but the tensor data)."""
     return dict(precision=side.precision, ffactor=side.ffactor, f_dev=side.f_dev,
                 n_in=side.n_in, n_out=side.n_out, value_scale_exp=side.value_scale_exp,
-                plan_kind=side.plan_kind,
+                plan_kind=side.plan_kind, contract=side.contract,
+                chunk_group=side.chunk_group,
                 info={f: getattr(side.info, f) for f in INFO_FIELDS},
                 tensors={k: (tuple(v.shape), str(v.dtype).replace("torch.", ""))
                          for k, v in side.tensors.items()})
@@ -613,5 +630,6 @@ def side_from_meta(meta: dict, tensors: dict) -> DeviceSide:
         setattr(info, f, v)
     side = DeviceSide(meta["precision"], meta["ffactor"], meta["f_dev"], meta["n_in"],
                       meta["n_out"], meta["value_scale_exp"], info, tensors,
-                      plan_kind=meta["plan_kind"])
+                      plan_kind=meta["plan_kind"], contract=meta.get("contract", False),
+                      chunk_group=meta.get("chunk_group", 1))
     return attach(side)

@@ -226,6 +226,7 @@ class DomainPartitionedSystem:
                 config.build == "streamed" or
                 (config.build == "auto" and 1.2 * g.num_angles * g.grid_n ** 2 > 4e9)):
             self._init_streamed(g, config, tomo, sino)
+            pipeline.configure_execution((self.forward, self.adjoint), config)
             return
         if self.rank == src:
             A = geo.build_system_matrix(g)
@@ -301,6 +302,7 @@ class DomainPartitionedSystem:
                                  fp_fwd, [s.elements for s in sino], self.rank, self.device)
         self.adjoint = _DistSide(mine[1], fp_adj[self.rank], self.col_owned, self.row_owned,
                                  fp_adj, [s.elements for s in tomo], self.rank, self.device)
+        pipeline.configure_execution((self.forward, self.adjoint), config)
 
     def _init_streamed(self, g, config, tomo, sino):
         """Every rank builds its own blocks (no whole matrix anywhere)."""

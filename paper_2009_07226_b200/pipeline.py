@@ -53,6 +53,14 @@ class SystemConfig:
                      or 4; lanes per row = record pieces / this; None = 2,
                      measured fastest with the 64-register K6 at F=16: one
                      lane per row in FP16, two in FP32).
+      contract       single precision: one FFMA per entry and slice instead
+                     of the reference's multiply-then-add; only with
+                     order="native", whose sums already differ from the
+                     reference's by rounding (None = off: measured 1% slower
+                     on the one-row-per-lane kernel, r01 probe).
+      chunk_group    F-chunks of a CTA tile launched back to back, so their
+                     CTAs share the tile's entry stream through L2 (16:
+                     measured 1-3% faster than 1 at c2, r01 probe).
       build          "streamed": never materialize the whole matrix -- the
                      projection format is built per chunk of views, the back
                      projection per band of voxels, from Siddon regenerated
@@ -76,6 +84,8 @@ class SystemConfig:
     smem_budget: int = matrixstore.SMEM_BUDGET
     build: str = "auto"
     pieces_per_lane: int | None = None
+    contract: bool | None = None
+    chunk_group: int = 16
 
     def __post_init__(self):
         if self.precision not in matrixstore.PRECISIONS:
@@ -90,6 +100,14 @@ class SystemConfig:
             raise ValueError("P_b and P_d must be >= 1")
         if self.build not in ("auto", "monolithic", "streamed"):
             raise ValueError(f"unknown build mode {self.build!r}")
+        if self.contract and self.order != "native":
+            raise ValueError("contract=True changes rounding; it needs order='native'")
+        if self.chunk_group < 1:
+            raise ValueError("chunk_group must be >= 1")
+
+    @property
+    def contract_effective(self) -> bool:
+        return bool(self.contract) and self.precision == "single"
 
 
 @dataclass
@@ -102,6 +120,13 @@ class _Side:
     ownership: list              # owned output ids per rank
     num_inputs: int
     num_outputs: int
+
+
+def configure_execution(sides, config) -> None:
+    """Apply the config's kernel execution knobs to every staged block."""
+    for side in sides:
+        for blk in side.blocks:
+            matrixstore.set_execution(blk, config.contract_effective, config.chunk_group)
 
 
 def _rows_per_warp(cfg) -> int:
@@ -202,6 +227,7 @@ class AssembledSystem:
             if geometry is None:
                 raise ValueError("data parallelism beyond P_d=1 needs a scan geometry")
             self._build_partitioned(ip, ix, v, n_rows, n_cols)
+        configure_execution((self.forward, self.adjoint), cfg)
 
     @classmethod
     def from_sides(cls, matrix, config: SystemConfig, geometry, forward_block, adjoint_block,
@@ -214,6 +240,7 @@ class AssembledSystem:
         n_rows, n_cols = int(matrix.num_rows), int(matrix.num_cols)
         self.forward = _Side([forward_block], [None], [None], [np.arange(n_rows)], n_cols, n_rows)
         self.adjoint = _Side([adjoint_block], [None], [None], [np.arange(n_cols)], n_rows, n_cols)
+        configure_execution((self.forward, self.adjoint), config)
         return self
 
     # -- construction ---------------------------------------------------------

@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--slices", type=int, default=None)
     ap.add_argument("--order", default="native")
     ap.add_argument("--ppl", type=int, default=None)
+    ap.add_argument("--groups", default="1", help="chunk_group values to sweep")
+    ap.add_argument("--contract", default="auto", help="auto | 0 | 1 | sweep")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.precision:
@@ -61,18 +63,38 @@ def main():
         x = (torch.rand((n_chunks, blk.n_in, blk.f_dev), device=dev) * 0.5).to(sd)
         y = torch.empty((n_chunks, blk.n_out, blk.f_dev), dtype=od, device=dev)
         fac = torch.ones(n_chunks, dtype=torch.float64, device=dev)
-        times = []
-        for _ in range(args.reps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            engine.apply_side(blk, x, y, row_stride=blk.f_dev, chunk_stride=blk.n_out * blk.f_dev,
-                              valid_cols=n_chunks * blk.f_dev, ffactor_out=blk.f_dev, factors=fac)
-            e1.record()
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1) / 1e3)
+        contracts = {"auto": [blk.contract], "0": [False], "1": [True],
+                     "sweep": [False, True]}[args.contract]
+        if prec != "single":
+            contracts = [False]
+        sweep = {}
+        ref_y = None
+        for cc in contracts:
+            for G in [int(v) for v in args.groups.split(",")]:
+                matrixstore.set_execution(blk, cc, G)
+                times = []
+                for _ in range(args.reps):
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    engine.apply_side(blk, x, y, row_stride=blk.f_dev,
+                                      chunk_stride=blk.n_out * blk.f_dev,
+                                      valid_cols=n_chunks * blk.f_dev, ffactor_out=blk.f_dev,
+                                      factors=fac)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    times.append(e0.elapsed_time(e1) / 1e3)
+                if ref_y is None:
+                    ref_y = y.clone()
+                    dev_rel = 0.0
+                else:
+                    dev_rel = float((y - ref_y).norm() / ref_y.norm())
+                sweep[f"contract={int(cc)},G={G}"] = {"ms": round(min(times) * 1e3, 3),
+                                                      "rel_vs_first": dev_rel}
         t = min(times)
         bytes_alg = blk.nnz * (2 + eb) * n_chunks + (blk.n_in + blk.n_out) * S * eb
-        out[name] = {"ms": [round(v * 1e3, 3) for v in times], "gflops": 2 * blk.nnz * S / t / 1e9,
+        out[name] = {"sweep": sweep, "ms": [round(v * 1e3, 3) for v in times],
+                     "gflops": 2 * blk.nnz * S / t / 1e9,
                      "alg_gbs": bytes_alg / t / 1e9, "bytes_alg": bytes_alg,
                      "padded_ratio": blk.padded_entries / blk.nnz,
                      "slots_per_nnz": int(blk.info.n_slots) / blk.nnz,
