@@ -107,6 +107,7 @@ typedef struct {
   int32_t value_bytes;
   double max_rel_quant_error;     /* PackReport.max_rel_error            */
   int64_t underflow_count;        /* PackReport.underflow_count          */
+  int32_t row_group;              /* values per slab position (G rows)   */
 } xct_format_info;
 
 int xct_format_build(int64_t n_rows, int64_t n_cols,
@@ -117,7 +118,7 @@ int xct_format_build(int64_t n_rows, int64_t n_cols,
                      const int32_t* h_key_tables, const int32_t* h_cta_table,
                      int64_t capacity, int precision, int value_scale_exp,
                      int sched_log2_pieces, int sched_log2_lanes,
-                     int n_threads, xct_format** out);
+                     int row_group, int n_threads, xct_format** out);
 int xct_format_get_info(const xct_format* f, xct_format_info* info);
 /* copies the format arrays into caller-provided host buffers sized from
  * xct_format_get_info; any pointer may be NULL to skip that array. */
@@ -128,7 +129,7 @@ int xct_format_export(const xct_format* f,
                       int64_t* h_slab_off /* [n_groups*warps_per_cta] */,
                       int32_t* h_slab_width /* [n_groups*warps_per_cta] */,
                       uint16_t* h_slots /* [n_padded] */,
-                      void* h_values /* [n_padded] of value_bytes */);
+                      void* h_values /* [n_padded*row_group] of value_bytes */);
 void xct_format_free(xct_format* f);
 
 /* stable counting transpose of a CSR block (src/matrixstore.py:189-201);
@@ -162,6 +163,7 @@ typedef struct {
   int32_t chunk_group; /* F-chunks of a tile launched adjacently (their CTAs
                           share the tile's entry stream through L2); the
                           largest power of two <= this dividing n_chunks */
+  int32_t row_group;   /* rows per unit of the format (xct_format_info)    */
 } xct_staged;
 
 typedef struct {

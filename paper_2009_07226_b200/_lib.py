@@ -27,7 +27,7 @@ class FormatInfo(C.Structure):
                 ("warps_per_cta", i64), ("n_groups", i64), ("n_slots", i64),
                 ("n_padded", i64), ("nnz", i64), ("max_group_slots", i64),
                 ("value_bytes", i32), ("max_rel_quant_error", f64),
-                ("underflow_count", i64)]
+                ("underflow_count", i64), ("row_group", i32)]
 
 
 class Staged(C.Structure):
@@ -36,7 +36,7 @@ class Staged(C.Structure):
                 ("d_cta_rows", vp), ("d_cta_group_ptr", vp), ("d_group_map_ptr", vp),
                 ("d_group_map", vp), ("d_slab_off", vp), ("d_slab_width", vp),
                 ("d_slots", vp), ("d_values", vp), ("max_group_slots", i64),
-                ("contract", i32), ("chunk_group", i32)]
+                ("contract", i32), ("chunk_group", i32), ("row_group", i32)]
 
 
 class Epilogue(C.Structure):
@@ -53,7 +53,7 @@ _SIGS = {
     "xct_csr_filter_cols": (i32, [vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp]),
     "xct_csr_filter_map": (i32, [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]),
     "xct_format_build": (i32, [i64, i64, vp, vp, vp, i64, i64, i64, vp, vp, vp, i64, i32,
-                               i32, i32, i32, i32, C.POINTER(vp)]),
+                               i32, i32, i32, i32, i32, C.POINTER(vp)]),
     "xct_format_get_info": (i32, [vp, C.POINTER(FormatInfo)]),
     "xct_format_export": (i32, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "xct_format_free": (None, [vp]),

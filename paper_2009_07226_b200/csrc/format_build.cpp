@@ -173,6 +173,7 @@ struct xct_format {
   std::unique_ptr<uint8_t[]> values;
   int64_t n_padded = 0;
   int vbytes = 0;
+  int row_group = 1;     // values per slab position (rows sharing an entry)
 };
 
 namespace {
@@ -208,14 +209,398 @@ struct PhaseLog {
 
 }  // namespace
 
+namespace {
+
+// ---- grouped rows (row_group G = 2 or 4) -----------------------------------
+// G consecutive thread-rows of a CTA form a unit owned by one lane set; the
+// unit walks the UNION of its rows' entries, so one staged-record read from
+// shared memory serves G rows (the shared-memory crossbar, not HBM, bounds
+// K6: SURVEY §7).  A union entry stores one slot and G values; a row absent
+// from the entry stores 0, and x*0 + acc == acc exactly, so every row's sum
+// is its own entries in stored order.  A column repeated inside one row gets
+// one extra union entry per repeat.  Union entries of a load group are
+// ordered by (key, column) -- ascending ray id per voxel for the back
+// projection -- then placed on slab steps by the bank schedule.
+// Slab layout per (group, warp): slots [width/4][units_per_warp][4] (as for
+// G = 1) and values [width/4][NV][units_per_warp][16 B], NV = 4*G*vbytes/16:
+// 16-byte piece k of a unit holds its value words k*epp.., word = entry*G +
+// row, so every 128-bit value load of a warp reads one contiguous run.
+struct UEnt {
+  int32_t key, col, dup, slot;
+  int64_t j[4];
+};
+
+int build_grouped(int64_t n_rows, int64_t n_cols, const int64_t* indptr, const int32_t* indices,
+                  const double* values, int64_t n_cta, int64_t rows_per_cta,
+                  int64_t rows_per_warp, const int32_t* cta_rows, const int32_t* key_tables,
+                  const int32_t* cta_table, int64_t capacity, int precision, int value_scale_exp,
+                  int sched_log2_pieces, int sched_log2_lanes, int G, int n_threads,
+                  xct_format** out) {
+  if (G != 2 && G != 4) return xct::fail(XCT_EINVAL, "format_build: row_group must be 1, 2 or 4");
+  if (n_rows < 0 || n_cols < 0 || n_cta < 0 || rows_per_cta < 1 || rows_per_warp < 1 ||
+      rows_per_cta % rows_per_warp || rows_per_warp % G)
+    return xct::fail(XCT_EINVAL, "format_build: bad shape arguments");
+  if (capacity < 1 || capacity > 65536)
+    return xct::fail(XCT_ESTAGE, "format_build: capacity must be in [1, 65536] slots");
+  if (precision != XCT_SINGLE && precision != XCT_MIXED)
+    return xct::fail(XCT_EINVAL, "format_build: grouped rows support single and mixed only");
+  if (!indptr || (!indices && indptr[n_rows] > 0) || !cta_rows || !key_tables || !cta_table)
+    return xct::fail(XCT_EINVAL, "format_build: null input array");
+  if (sched_log2_pieces < 0)
+    return xct::fail(XCT_EINVAL, "format_build: grouped rows need the bank schedule");
+  const int64_t warps = rows_per_cta / rows_per_warp;
+  const int64_t upw = rows_per_warp / G;            // units per warp
+  const int64_t upc = rows_per_cta / G;             // units per CTA
+  const int vbytes = precision == XCT_SINGLE ? 4 : 2;
+  if (sched_log2_lanes < 0 || sched_log2_lanes > sched_log2_pieces ||
+      (32 >> sched_log2_lanes) != upw)
+    return xct::fail(XCT_EINVAL, "format_build: schedule lanes do not match units per warp");
+  BankModel bank;
+  bank.init(sched_log2_pieces, sched_log2_lanes);
+  const int64_t rq = bank.on() ? bank.rq : upw;
+  PhaseLog plog;
+  std::vector<CtaPlan> plans(n_cta);
+  std::mutex err_mu;
+  int err = XCT_OK;
+  std::string err_msg;
+
+  // ---- phase A: footprint, load groups, union widths per (group, warp) ----
+  parallel_for(n_cta, n_threads, [&](int64_t b) {
+    CtaPlan& P = plans[b];
+    const int32_t* keys = key_tables + (int64_t)cta_table[b] * n_cols;
+    static thread_local std::vector<int64_t> fstamp, ustamp, rstamp;
+    static thread_local int64_t gen = 0;
+    static thread_local std::vector<int32_t> group_of, cls_of;
+    if ((int64_t)fstamp.size() < n_cols) {
+      fstamp.assign(n_cols, -1); ustamp.assign(n_cols, -1); rstamp.assign(n_cols, -1);
+      group_of.assign(n_cols, 0); cls_of.assign(n_cols, 0);
+    }
+    const int64_t fm = ++gen;
+    std::vector<KC> all;
+    for (int64_t t = 0; t < rows_per_cta; ++t) {
+      int32_t r = cta_rows[b * rows_per_cta + t];
+      if (r < 0) continue;
+      for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) {
+        const int32_t col = indices[j];
+        if (fstamp[col] == fm) continue;
+        fstamp[col] = fm;
+        all.push_back({keys[col], col});
+      }
+    }
+    std::sort(all.begin(), all.end(), kc_less);
+    P.foot.swap(all);
+    int64_t cur = 0, i = 0, n = (int64_t)P.foot.size();
+    P.gstart.push_back(0);
+    while (i < n) {
+      int64_t j = i;
+      while (j < n && P.foot[j].key == P.foot[i].key) ++j;
+      int64_t m = j - i;
+      if (m > capacity) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        err = XCT_ESTAGE;
+        err_msg = "format_build: one staging key needs " + std::to_string(m) +
+                  " slots, capacity is " + std::to_string(capacity);
+        return;
+      }
+      if (cur + m > capacity) { P.gstart.push_back(i); cur = 0; }
+      cur += m;
+      i = j;
+    }
+    if (n > 0) P.gstart.push_back(n);
+    else P.gstart.clear();
+    const int64_t ng = P.gstart.empty() ? 0 : (int64_t)P.gstart.size() - 1;
+    P.width.assign(ng * warps, 0);
+    for (int64_t g = 0; g < ng; ++g)
+      for (int64_t p = P.gstart[g]; p < P.gstart[g + 1]; ++p) {
+        group_of[P.foot[p].col] = (int32_t)g;
+        cls_of[P.foot[p].col] = bank.on() ? bank.cls(p - P.gstart[g]) : 0;
+      }
+    std::vector<int32_t> cnt(ng), ccnt(ng * 8);
+    for (int64_t u = 0; u < upc; ++u) {
+      const int64_t w = u / upw;
+      if (u % rq == 0) std::fill(ccnt.begin(), ccnt.end(), 0);
+      std::fill(cnt.begin(), cnt.end(), 0);
+      const int64_t um = ++gen;
+      for (int gi = 0; gi < G; ++gi) {
+        const int32_t r = cta_rows[b * rows_per_cta + u * G + gi];
+        if (r < 0) continue;
+        const int64_t rm = ++gen;
+        for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) {
+          const int32_t col = indices[j];
+          bool fresh;
+          if (rstamp[col] == rm) {
+            fresh = true;                          // repeat inside the row
+          } else {
+            rstamp[col] = rm;
+            fresh = ustamp[col] != um;
+            ustamp[col] = um;
+          }
+          if (fresh) {
+            ++cnt[group_of[col]];
+            ++ccnt[group_of[col] * 8 + cls_of[col]];
+          }
+        }
+      }
+      for (int64_t g = 0; g < ng; ++g) {
+        int32_t pw = (cnt[g] + 3) & ~3;
+        if (pw > P.width[g * warps + w]) P.width[g * warps + w] = pw;
+      }
+      if (u % rq == rq - 1 || u == upc - 1) {
+        for (int64_t g = 0; g < ng; ++g)
+          for (int c = 0; c < 8; ++c) {
+            int32_t pw = (ccnt[g * 8 + c] + 3) & ~3;
+            if (pw > P.width[g * warps + w]) P.width[g * warps + w] = pw;
+          }
+      }
+    }
+  });
+  if (err) return xct::fail(err, err_msg);
+  plog.lap("A(grouped)");
+
+  // ---- phase B: global offsets ---------------------------------------------
+  xct_format* F = new (std::nothrow) xct_format();
+  if (!F) return xct::fail(XCT_ENOMEM, "format_build: out of host memory");
+  F->cta_group_ptr.assign(n_cta + 1, 0);
+  int64_t n_groups = 0, n_slots = 0, n_padded = 0, max_gs = 0;
+  for (int64_t b = 0; b < n_cta; ++b) {
+    int64_t ng = plans[b].gstart.empty() ? 0 : (int64_t)plans[b].gstart.size() - 1;
+    n_groups += ng;
+    F->cta_group_ptr[b + 1] = (int32_t)n_groups;
+    n_slots += (int64_t)plans[b].foot.size();
+    for (int64_t g = 0; g < ng; ++g)
+      max_gs = std::max(max_gs, plans[b].gstart[g + 1] - plans[b].gstart[g]);
+    for (int32_t w : plans[b].width) n_padded += (int64_t)w * upw;
+  }
+  if (n_groups > INT32_MAX) { delete F; return xct::fail(XCT_EINVAL, "format_build: too many groups"); }
+  try {
+    F->group_map_ptr.assign(n_groups + 1, 0);
+    F->group_map.assign(n_slots, 0);
+    F->slab_off.assign(n_groups * warps, 0);
+    F->slab_width.assign(n_groups * warps, 0);
+    F->slots.reset(new uint16_t[std::max<int64_t>(n_padded, 1)]);
+    F->values.reset(new uint8_t[std::max<int64_t>(n_padded, 1) * vbytes * G]);
+    F->n_padded = n_padded;
+    F->vbytes = vbytes;
+    F->row_group = G;
+  } catch (...) {
+    delete F;
+    return xct::fail(XCT_ENOMEM, "format_build: out of host memory");
+  }
+  std::vector<int64_t> cta_slot0(n_cta + 1, 0), cta_e0(n_cta + 1, 0);
+  {
+    int64_t gi = 0, so = 0, eo = 0;
+    for (int64_t b = 0; b < n_cta; ++b) {
+      cta_slot0[b] = so;
+      cta_e0[b] = eo;
+      const CtaPlan& P = plans[b];
+      int64_t ng = P.gstart.empty() ? 0 : (int64_t)P.gstart.size() - 1;
+      for (int64_t g = 0; g < ng; ++g) {
+        so += P.gstart[g + 1] - P.gstart[g];
+        F->group_map_ptr[gi + g + 1] = so;
+      }
+      for (int64_t w = 0; w < warps; ++w)
+        for (int64_t g = 0; g < ng; ++g) {
+          F->slab_off[(gi + g) * warps + w] = eo;
+          F->slab_width[(gi + g) * warps + w] = P.width[g * warps + w];
+          eo += (int64_t)P.width[g * warps + w] * upw;
+        }
+      gi += ng;
+    }
+    cta_e0[n_cta] = eo;
+  }
+  plog.lap("B(grouped)");
+
+  // ---- phase C: fill maps and slabs ----------------------------------------
+  const double scale = std::ldexp(1.0, value_scale_exp);
+  std::vector<double> worst(n_cta, 0.0);
+  std::vector<int64_t> under(n_cta, 0);
+  parallel_for(n_cta, n_threads, [&](int64_t b) {
+    if (err) return;
+    const CtaPlan& P = plans[b];
+    const int32_t* keys = key_tables + (int64_t)cta_table[b] * n_cols;
+    const int64_t g0 = F->cta_group_ptr[b];
+    std::memset(F->slots.get() + cta_e0[b], 0, (size_t)(cta_e0[b + 1] - cta_e0[b]) * 2);
+    std::memset(F->values.get() + cta_e0[b] * vbytes * G, 0,
+                (size_t)(cta_e0[b + 1] - cta_e0[b]) * vbytes * G);
+    for (size_t i = 0; i < P.foot.size(); ++i) F->group_map[cta_slot0[b] + i] = P.foot[i].col;
+    const int64_t ng = P.gstart.empty() ? 0 : (int64_t)P.gstart.size() - 1;
+    static thread_local std::vector<int32_t> slot_of, group_of, uidx;
+    static thread_local std::vector<int64_t> ustamp, rstamp;
+    static thread_local int64_t gen = 0;
+    if ((int64_t)slot_of.size() < n_cols) {
+      slot_of.assign(n_cols, 0); group_of.assign(n_cols, 0); uidx.assign(n_cols, 0);
+      ustamp.assign(n_cols, -1); rstamp.assign(n_cols, -1);
+    }
+    for (int64_t g = 0; g < ng; ++g)
+      for (int64_t p = P.gstart[g]; p < P.gstart[g + 1]; ++p) {
+        group_of[P.foot[p].col] = (int32_t)g;
+        slot_of[P.foot[p].col] = (int32_t)(p - P.gstart[g]);
+      }
+    // union entries of every unit, sorted, with per-(unit, group) offsets
+    std::vector<UEnt> flat;
+    std::vector<int64_t> gofs((size_t)(ng + 1) * upc, 0);
+    std::vector<UEnt> list;
+    for (int64_t u = 0; u < upc; ++u) {
+      list.clear();
+      const int64_t um = ++gen;
+      int32_t dupc = 0;
+      for (int gi = 0; gi < G; ++gi) {
+        const int32_t r = cta_rows[b * rows_per_cta + u * G + gi];
+        if (r < 0) continue;
+        const int64_t rm = ++gen;
+        for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) {
+          const int32_t col = indices[j];
+          if (rstamp[col] != rm && ustamp[col] == um) {
+            rstamp[col] = rm;
+            list[uidx[col]].j[gi] = j;
+            continue;
+          }
+          UEnt e{keys[col], col, 0, slot_of[col], {-1, -1, -1, -1}};
+          e.j[gi] = j;
+          if (rstamp[col] == rm) {
+            e.dup = ++dupc;                         // repeat inside the row
+          } else {
+            rstamp[col] = rm;
+            ustamp[col] = um;
+            uidx[col] = (int32_t)list.size();
+          }
+          list.push_back(e);
+        }
+      }
+      std::sort(list.begin(), list.end(), [](const UEnt& a, const UEnt& c) {
+        if (a.key != c.key) return a.key < c.key;
+        if (a.col != c.col) return a.col < c.col;
+        return a.dup < c.dup;
+      });
+      const int64_t base = (int64_t)flat.size();
+      int64_t at = 0;
+      const int64_t m = (int64_t)list.size();
+      for (int64_t g = 0; g <= ng; ++g) {
+        while (g < ng && at < m && group_of[list[at].col] < g) ++at;
+        gofs[(size_t)u * (ng + 1) + g] = base + (g < ng ? at : m);
+      }
+      flat.insert(flat.end(), list.begin(), list.end());
+    }
+    double wmax = 0.0;
+    int64_t nunder = 0;
+    auto write = [&](int64_t gg, int64_t w, int64_t uin, int64_t n, const UEnt* E, int32_t slot) {
+      const int64_t at = F->slab_off[gg * warps + w] + ((n >> 2) * upw + uin) * 4 + (n & 3);
+      F->slots[at] = (uint16_t)slot;
+      if (!E) return;                          // padding: values stay 0
+      // values of a step: [NV][units][16 B]; piece k of a unit holds its
+      // words k*epp .. k*epp+epp-1, word = entry*G + row (so each 128-bit
+      // load instruction of a warp reads one contiguous run)
+      const int64_t epp = 16 / vbytes;
+      const int64_t step0 = F->slab_off[gg * warps + w] + (n >> 2) * upw * 4;
+      for (int gi = 0; gi < G; ++gi) {
+        const int64_t j = E->j[gi];
+        if (j < 0) continue;
+        const double v = values[j] * scale;
+        double back;
+        const int64_t wd = (n & 3) * G + gi;
+        const int64_t vi = step0 * G + ((wd / epp) * upw + uin) * epp + wd % epp;
+        uint8_t* dst = F->values.get() + vi * vbytes;
+        if (precision == XCT_SINGLE) {
+          float f = (float)v;
+          std::memcpy(dst, &f, 4);
+          back = (double)f;
+        } else {
+          uint16_t h = f64_to_f16(v);
+          std::memcpy(dst, &h, 2);
+          back = f16_to_f64(h);
+        }
+        if (v != 0.0) {
+          if (back == 0.0) ++nunder;
+          double rel = std::fabs(back - v) / std::fabs(v);
+          if (rel > wmax) wmax = rel;
+        }
+      }
+    };
+    Colorer colorer;
+    std::vector<int32_t> step_slot;
+    std::vector<std::pair<int64_t, const UEnt*>> owner;
+    std::vector<char> used;
+    for (int64_t g = 0; g < ng; ++g) {
+      const int64_t gg = g0 + g;
+      for (int64_t w = 0; w < warps; ++w) {
+        const int64_t width = F->slab_width[gg * warps + w];
+        for (int64_t q0 = 0; q0 < upw; q0 += rq) {
+          colorer.reset((int)rq, 8, (int)width);
+          step_slot.assign(width, -1);
+          owner.clear();
+          for (int64_t rr = 0; rr < rq; ++rr) {
+            const int64_t u = w * upw + q0 + rr;
+            const int64_t a = gofs[(size_t)u * (ng + 1) + g], e = gofs[(size_t)u * (ng + 1) + g + 1];
+            for (int64_t k = a; k < e; ++k) {
+              if (!colorer.add((int)rr, bank.cls(flat[k].slot))) {
+                std::lock_guard<std::mutex> lk(err_mu);
+                err = XCT_EINVAL;
+                err_msg = "format_build: bank schedule exceeded the slab width";
+                return;
+              }
+              owner.push_back({q0 + rr, &flat[k]});
+            }
+          }
+          used.assign((size_t)rq * width, 0);
+          for (size_t e = 0; e < owner.size(); ++e) {
+            const int64_t uin = owner[e].first;
+            const int64_t n = colorer.col[e];
+            write(gg, w, uin, n, owner[e].second, owner[e].second->slot);
+            used[(size_t)(uin - q0) * width + n] = 1;
+            if (step_slot[n] < 0) step_slot[n] = owner[e].second->slot;
+          }
+          for (int64_t rr = 0; rr < rq; ++rr)
+            for (int64_t n = 0; n < width; ++n)
+              if (!used[(size_t)rr * width + n] && step_slot[n] > 0)
+                write(gg, w, q0 + rr, n, nullptr, step_slot[n]);
+        }
+      }
+    }
+    worst[b] = wmax;
+    under[b] = nunder;
+  });
+  if (err) {
+    delete F;
+    return xct::fail(err, err_msg);
+  }
+  plog.lap("C(grouped)");
+  F->info.n_cta = n_cta;
+  F->info.rows_per_cta = rows_per_cta;
+  F->info.rows_per_warp = rows_per_warp;
+  F->info.warps_per_cta = warps;
+  F->info.n_groups = n_groups;
+  F->info.n_slots = n_slots;
+  F->info.n_padded = n_padded;
+  F->info.nnz = indptr[n_rows] - indptr[0];
+  F->info.max_group_slots = max_gs;
+  F->info.value_bytes = vbytes;
+  F->info.row_group = G;
+  double wm = 0.0;
+  int64_t un = 0;
+  for (int64_t b = 0; b < n_cta; ++b) { wm = std::max(wm, worst[b]); un += under[b]; }
+  F->info.max_rel_quant_error = wm;
+  F->info.underflow_count = un;
+  *out = F;
+  return XCT_OK;
+}
+
+}  // namespace
+
+
 extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* indptr,
                                 const int32_t* indices, const double* values,
                                 int64_t n_cta, int64_t rows_per_cta, int64_t rows_per_warp,
                                 const int32_t* cta_rows, const int32_t* key_tables,
                                 const int32_t* cta_table, int64_t capacity, int precision,
                                 int value_scale_exp, int sched_log2_pieces,
-                                int sched_log2_lanes, int n_threads, xct_format** out) {
+                                int sched_log2_lanes, int row_group, int n_threads,
+                                xct_format** out) {
   if (!out) return xct::fail(XCT_EINVAL, "format_build: null output handle");
+  if (row_group != 1)
+    return build_grouped(n_rows, n_cols, indptr, indices, values, n_cta, rows_per_cta,
+                         rows_per_warp, cta_rows, key_tables, cta_table, capacity, precision,
+                         value_scale_exp, sched_log2_pieces, sched_log2_lanes, row_group,
+                         n_threads, out);
   *out = nullptr;
   if (n_rows < 0 || n_cols < 0 || n_cta < 0 || rows_per_cta < 1 || rows_per_warp < 1 ||
       rows_per_cta % rows_per_warp)
@@ -536,6 +921,7 @@ extern "C" int xct_format_build(int64_t n_rows, int64_t n_cols, const int64_t* i
   F->info.nnz = indptr[n_rows] - indptr[0];
   F->info.max_group_slots = max_gs;
   F->info.value_bytes = vbytes;
+  F->info.row_group = 1;
   double wm = 0.0;
   int64_t un = 0;
   for (int64_t b = 0; b < n_cta; ++b) { wm = std::max(wm, worst[b]); un += under[b]; }
@@ -573,7 +959,7 @@ extern "C" int xct_format_export(const xct_format* f, int32_t* cta_group_ptr,
     });
   };
   pcp(slots, f->slots.get(), (size_t)f->n_padded * 2);
-  pcp(values, f->values.get(), (size_t)f->n_padded * f->vbytes);
+  pcp(values, f->values.get(), (size_t)f->n_padded * f->vbytes * f->row_group);
   return XCT_OK;
 }
 

@@ -487,6 +487,242 @@ int launch_npl(const Params& p, int npl, int64_t n_chunks, int threads, int64_t 
   }
 }
 
+// ---- grouped rows: one union entry feeds G rows (format row_group = G) ----
+// A unit of G rows walks the union of its rows' entries: every staged record
+// read from shared memory (the K6 bottleneck) is used by G rows, with a
+// stored 0 for rows that lack the column (x*0 + acc == acc exactly).  Step =
+// 4 union entries: 4 u16 offsets (one 64-bit load) + 4*G values (G single /
+// G/2 mixed 128-bit loads), a register ring as deep as 128 registers allow.
+
+template <int PREC, int G> struct GStep;
+
+template <int G> struct GStep<XCT_SINGLE, G> {
+  static constexpr int NV = G;                      // 4 entries * G * 4 B / 16
+  uint2 s;
+  uint4 v[NV];
+  // vb: 16-byte piece index of this unit's first value piece in the step;
+  // piece k sits upw pieces further (values [NV][units][16 B] per step)
+  __device__ void load(const uint16_t* sl, const void* vv, int64_t idx, int64_t vb, int upw,
+                       uint64_t pol) {
+    s = ld_stream_u2(sl + idx, pol);
+    const uint4* pv = reinterpret_cast<const uint4*>(vv) + vb;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = ld_stream_u4(pv + (int64_t)k * upw, pol);
+  }
+  __device__ uint32_t off(int e) const {
+    uint32_t q = e < 2 ? s.x : s.y;
+    return (e & 1) ? (q >> 16) : (q & 0xffffu);
+  }
+  __device__ uint32_t word(int w) const {
+    const uint4& q = v[w >> 2];
+    return (w & 3) == 0 ? q.x : (w & 3) == 1 ? q.y : (w & 3) == 2 ? q.z : q.w;
+  }
+  __device__ float val(int e, int gi) const { return __uint_as_float(word(e * G + gi)); }
+};
+
+template <int G> struct GStep<XCT_MIXED, G> {
+  static constexpr int NV = G / 2;                  // 4 entries * G * 2 B / 16
+  uint2 s;
+  uint4 v[NV];
+  // vb: 16-byte piece index of this unit's first value piece in the step;
+  // piece k sits upw pieces further (values [NV][units][16 B] per step)
+  __device__ void load(const uint16_t* sl, const void* vv, int64_t idx, int64_t vb, int upw,
+                       uint64_t pol) {
+    s = ld_stream_u2(sl + idx, pol);
+    const uint4* pv = reinterpret_cast<const uint4*>(vv) + vb;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = ld_stream_u4(pv + (int64_t)k * upw, pol);
+  }
+  __device__ uint32_t off(int e) const {
+    uint32_t q = e < 2 ? s.x : s.y;
+    return (e & 1) ? (q >> 16) : (q & 0xffffu);
+  }
+  __device__ unsigned short val(int e, int gi) const {
+    const int h = e * G + gi, w = h >> 1;
+    const uint4& q = v[w >> 2];
+    const uint32_t x = (w & 3) == 0 ? q.x : (w & 3) == 1 ? q.y : (w & 3) == 2 ? q.z : q.w;
+    return (unsigned short)((h & 1) ? (x >> 16) : (x & 0xffffu));
+  }
+};
+
+template <int NPL, int G, typename A, typename St>
+__device__ __forceinline__ void consume_g(A (&acc)[G], const St& cur, const uint32_t (&pb)[NPL]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t off = cur.off(e);
+#pragma unroll
+    for (int qq = 0; qq < NPL; ++qq) {
+      const uint4 r = lds128(pb[qq] + off);
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi) acc[gi].fma(qq, r, cur.val(e, gi));
+    }
+  }
+}
+
+// ring depth: as deep as the registers allow (values of a step: 4*NV regs)
+template <int PREC, int NPL, int G> struct RingDepth {
+  static constexpr int nv = GStep<PREC, G>::NV;
+  static constexpr int acc = NPL * (PREC == XCT_MIXED ? 8 : 4) * G;
+  static constexpr int value = acc + 4 * nv * 3 <= 72 ? 4 : acc + 4 * nv * 2 <= 80 ? 3 : 2;
+};
+
+template <int PREC, int NPL, int G, bool CONTRACT>
+__global__ void __launch_bounds__(512) spmm_grouped_kernel(const Params p) {
+  using A = Acc<PREC, NPL, CONTRACT>;
+  using St = GStep<PREC, G>;
+  constexpr int V = A::V;
+  extern __shared__ uint4 stage[];
+  const int64_t id = blockIdx.x;
+  const int CG = p.chunk_group;
+  const int b = (int)((id / CG) % p.n_cta);
+  const int chunk = (int)(id / ((int64_t)CG * p.n_cta)) * CG + (int)(id % CG);
+  const int lg = p.log2_lanes;               // lanes per unit = 1 << lg
+  const int lp = p.log2_pieces;
+  const int upw = 32 >> lg;                  // units per warp
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int uin = lane >> lg, sub = lane & ((1 << lg) - 1);
+  const uint4* xb = p.x + (int64_t)chunk * p.n_in * (1 << lp);
+  const uint64_t pol_x = policy_evict_last(), pol_e = policy_evict_first();
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(stage);
+  const uint32_t bb = buffer_bytes(lp, p.plane_slots);
+  uint32_t pbase[NPL];
+#pragma unroll
+  for (int qq = 0; qq < NPL; ++qq) pbase[qq] = plane_base(sub * NPL + qq, lp, p.plane_slots);
+
+  A acc[G];
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) acc[gi].zero();
+  const int g0 = p.cta_group_ptr[b], g1 = p.cta_group_ptr[b + 1];
+  const int64_t step = (int64_t)upw * 4;
+  int64_t at = (g0 < g1 ? p.slab_off[(int64_t)g0 * p.warps_per_cta + warp] : 0) +
+               (int64_t)uin * 4;
+  // value pieces: a step of the warp is NV*upw pieces; this unit's first
+  // piece of the step starting at position s0 (= at - 4*uin) is s0/4*NV + uin
+  const int64_t vstep = (int64_t)St::NV * upw;
+  int64_t vb = (at - 4 * uin) / 4 * St::NV + uin;
+  constexpr int D = RingDepth<PREC, NPL, G>::value;
+  // The warp's steps of all groups form one stream: r[i] holds the steps
+  // k = i mod D, and the load of step k + D is issued as soon as step k is
+  // consumed, straight through group boundaries (one copy of the unrolled
+  // body -- phase-specialised copies overflow the instruction cache).
+  St r[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) r[i].load(p.slots, p.values, at + i * step, vb + i * vstep, upw, pol_e);
+  int32_t* const maps = reinterpret_cast<int32_t*>(
+      reinterpret_cast<char*>(stage) + 2 * (size_t)bb);
+  int32_t* const map0 = maps;
+  int32_t* const map1 = maps + p.plane_slots;
+  int64_t mp0 = g0 < g1 ? p.group_map_ptr[g0] : 0;
+  int64_t mp1 = g0 < g1 ? p.group_map_ptr[g0 + 1] : 0;
+  int64_t mp2 = g0 + 1 < g1 ? p.group_map_ptr[g0 + 2] : mp1;
+  if (g0 < g1) {
+    map_fill(p, map0, mp0, (int)(mp1 - mp0));
+    if (g0 + 1 < g1) map_fill(p, map1, mp1, (int)(mp2 - mp1));
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    stage_fill(p, xb, s0, map0, (int)(mp1 - mp0), lp, pol_x);
+  }
+  cp_async_commit();
+  int g = g0 - 1, left = 0;
+  uint32_t pb[NPL];
+#pragma unroll
+  for (int qq = 0; qq < NPL; ++qq) pb[qq] = s0 + pbase[qq];
+  // enter group gn: its records are staged (barrier), start staging gn + 1
+  auto enter = [&](int gn) {
+    const int odd = (gn - g0) & 1;
+    left = p.slab_width[(int64_t)gn * p.warps_per_cta + warp] >> 2;
+    const int64_t mp3 = gn + 3 <= g1 ? p.group_map_ptr[min(gn + 3, g1)] : mp2;
+    cp_async_wait_all();
+    __syncthreads();
+    if (gn + 1 < g1)
+      stage_fill(p, xb, s0 + (odd ? 0u : bb), odd ? map0 : map1, (int)(mp2 - mp1), lp, pol_x);
+    if (gn + 2 < g1)
+      map_fill(p, odd ? map1 : map0, mp2, (int)(mp3 - mp2));
+    cp_async_commit();
+    mp1 = mp2;
+    mp2 = mp3;
+#pragma unroll
+    for (int qq = 0; qq < NPL; ++qq) pb[qq] = s0 + (odd ? bb : 0u) + pbase[qq];
+  };
+  for (;;) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      while (left == 0) {
+        if (++g >= g1) goto done;
+        enter(g);
+      }
+      consume_g<NPL, G>(acc, r[i], pb);
+      r[i].load(p.slots, p.values, at + D * step, vb + D * vstep, upw, pol_e);
+      at += step;
+      vb += vstep;
+      --left;
+    }
+  }
+done:
+  cp_async_wait_all();
+
+  // ---- epilogue: G rows per unit ------------------------------------------
+  double sq = 0.0;
+  const float sc = ldexpf(1.0f, -p.scale_exp);
+  const float f = p.factors ? (float)p.factors[chunk] : 1.0f;
+  const int j0 = sub * NPL * V;
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) {
+    const int row = p.cta_rows[(int64_t)b * p.rows_per_cta + (warp * upw + uin) * G + gi];
+    if (row < 0) continue;
+    float* out = (float*)p.out + (int64_t)row * p.row_stride + (int64_t)chunk * p.chunk_stride;
+#pragma unroll
+    for (int i = 0; i < NPL * V; ++i) {
+      const int j = j0 + i;
+      if (j < p.ffactor && chunk * p.ffactor + j < p.valid_cols) {
+        const float v = acc[gi].out(i, sc) * f;
+        out[j] = v;
+        sq += (double)v * (double)v;
+      }
+    }
+  }
+  if (p.dot_partials) {
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    __shared__ double red[32];
+    if (lane == 0) red[warp] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      p.dot_partials[(int64_t)chunk * p.n_cta + b] = t;
+    }
+  }
+}
+
+template <int PREC, int NPL, int G, bool CONTRACT>
+int launch_grouped(const Params& p, int64_t n_chunks, int threads, int64_t smem, cudaStream_t s) {
+  static int configured = -1;
+  if (configured < (int)smem) {
+    cudaError_t e = cudaFuncSetAttribute(spmm_grouped_kernel<PREC, NPL, G, CONTRACT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+      return xct::fail(XCT_ECUDA, std::string("spmm smem attribute: ") + cudaGetErrorString(e));
+    configured = (int)smem;
+  }
+  if (threads > 512) return xct::fail(XCT_EINVAL, "spmm: grouped rows need <= 16 warps per CTA");
+  const int64_t n_blocks = (int64_t)p.n_cta * n_chunks;
+  if (n_blocks > 0x7fffffffLL) return xct::fail(XCT_EINVAL, "spmm: grid too large");
+  spmm_grouped_kernel<PREC, NPL, G, CONTRACT><<<(unsigned)n_blocks, threads, smem, s>>>(p);
+  XCT_CUDA_CHECK_LAUNCH("spmm_grouped");
+  return XCT_OK;
+}
+
+template <int PREC, bool CONTRACT>
+int launch_grouped_npl(const Params& p, int npl, int G, int64_t n_chunks, int threads,
+                       int64_t smem, cudaStream_t s) {
+  if (npl == 1 && G == 2) return launch_grouped<PREC, 1, 2, CONTRACT>(p, n_chunks, threads, smem, s);
+  if (npl == 1 && G == 4) return launch_grouped<PREC, 1, 4, CONTRACT>(p, n_chunks, threads, smem, s);
+  if (npl == 2 && G == 2) return launch_grouped<PREC, 2, 2, CONTRACT>(p, n_chunks, threads, smem, s);
+  if (npl == 2 && G == 4) return launch_grouped<PREC, 2, 4, CONTRACT>(p, n_chunks, threads, smem, s);
+  return xct::fail(XCT_EINVAL, "spmm: grouped rows need G in {2, 4} and 1 or 2 pieces per lane");
+}
+
 }  // namespace
 
 extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int64_t n_in,
@@ -495,7 +731,10 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   if (!a || !ep || !d_x || !ep->d_out) return xct::fail(XCT_EINVAL, "spmm: null argument");
   if (precision < 0 || precision > 3) return xct::fail(XCT_EINVAL, "spmm: bad precision");
   if (ep->accumulate) return xct::fail(XCT_EINVAL, "spmm: accumulate mode is reserved");
-  const bool packed = precision == XCT_HALF || precision == XCT_MIXED;
+  const int G = a->row_group > 1 ? a->row_group : 1;
+  if (G > 1 && precision != XCT_SINGLE && precision != XCT_MIXED)
+    return xct::fail(XCT_EINVAL, "spmm: grouped rows support single and mixed only");
+  const bool packed = (precision == XCT_HALF || precision == XCT_MIXED) && G == 1;
   if (!a->d_values || (!packed && !a->d_slots))
     return xct::fail(XCT_EINVAL, "spmm: missing entry arrays");
   const int vbytes = precision == XCT_DOUBLE ? 8 : precision == XCT_SINGLE ? 4 : 2;
@@ -504,18 +743,20 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
     return xct::fail(XCT_EINVAL, "spmm: f_dev*elem_bytes must be a power of two in [16, 512]");
   int lp = 0;
   while ((16 << lp) < rec) ++lp;                      // pieces per record = 1 << lp
-  int lg = 0;                                         // lanes per row = 1 << lg
-  while ((32 >> lg) > a->rows_per_warp && lg < 5) ++lg;
-  if ((32 >> lg) != a->rows_per_warp || lg > lp)
-    return xct::fail(XCT_EINVAL, "spmm: rows_per_warp must be 32 / lanes with lanes <= pieces");
+  if (a->rows_per_warp % G) return xct::fail(XCT_EINVAL, "spmm: rows_per_warp % row_group");
+  const int64_t upw = a->rows_per_warp / G;         // units (row groups) per warp
+  int lg = 0;                                         // lanes per unit = 1 << lg
+  while ((32 >> lg) > upw && lg < 5) ++lg;
+  if ((32 >> lg) != upw || lg > lp)
+    return xct::fail(XCT_EINVAL, "spmm: units per warp must be 32 / lanes with lanes <= pieces");
   const int npl = 1 << (lp - lg);
   if (a->n_cta == 0 || n_chunks == 0) return XCT_OK;
   if (n_chunks > 65535) return xct::fail(XCT_EINVAL, "spmm: too many chunks for one launch");
   if (a->contract && precision != XCT_SINGLE)
     return xct::fail(XCT_EINVAL, "spmm: contract applies to single precision only");
   // largest power of two <= chunk_group that divides n_chunks
-  int G = 1;
-  while (G * 2 <= a->chunk_group && n_chunks % (G * 2) == 0) G *= 2;
+  int CG = 1;
+  while (CG * 2 <= a->chunk_group && n_chunks % (CG * 2) == 0) CG *= 2;
   const int threads = (int)(a->warps_per_cta * 32);
   if (threads < 32 || threads > 1024) return xct::fail(XCT_EINVAL, "spmm: CTA must have 1..32 warps");
   const int64_t plane_slots = (a->max_group_slots + 7) & ~(int64_t)7;
@@ -542,7 +783,7 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   p.log2_pieces = lp;
   p.n_cta = (int32_t)a->n_cta;
   p.plane_slots = (int32_t)plane_slots;
-  p.chunk_group = G;
+  p.chunk_group = CG;
   p.n_chunks = (int32_t)n_chunks;
   p.out = ep->d_out;
   p.row_stride = ep->row_stride;
@@ -553,6 +794,13 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   p.factors = ep->d_factors;
   p.dot_partials = ep->d_dot_partials;
   cudaStream_t s = (cudaStream_t)stream;
+  if (G > 1) {
+    if (precision == XCT_MIXED)
+      return launch_grouped_npl<XCT_MIXED, false>(p, npl, G, n_chunks, threads, smem_bytes, s);
+    return a->contract
+               ? launch_grouped_npl<XCT_SINGLE, true>(p, npl, G, n_chunks, threads, smem_bytes, s)
+               : launch_grouped_npl<XCT_SINGLE, false>(p, npl, G, n_chunks, threads, smem_bytes, s);
+  }
   switch (precision) {
     case XCT_DOUBLE: return launch_npl<XCT_DOUBLE>(p, npl, n_chunks, threads, smem_bytes, s);
     case XCT_SINGLE:

@@ -56,11 +56,17 @@ class SystemConfig:
       contract       single precision: one FFMA per entry and slice instead
                      of the reference's multiply-then-add; only with
                      order="native", whose sums already differ from the
-                     reference's by rounding (None = off: measured 1% slower
-                     on the one-row-per-lane kernel, r01 probe).
+                     reference's by rounding (None = on for grouped-row
+                     blocks, where it is 20% faster; off for one row per lane
+                     set, where it measured 1% slower).
       chunk_group    F-chunks of a CTA tile launched back to back, so their
                      CTAs share the tile's entry stream through L2 (16:
                      measured 1-3% faster than 1 at c2, r01 probe).
+      row_group      rows per lane set of K6 (1, 2 or 4; native order,
+                     single/mixed): the lanes walk the union of the rows'
+                     entries, so each staged record read from shared memory
+                     serves row_group rows (2 views x 2 detectors for A,
+                     2 x 2 voxels for A^T).
       build          "streamed": never materialize the whole matrix -- the
                      projection format is built per chunk of views, the back
                      projection per band of voxels, from Siddon regenerated
@@ -86,6 +92,7 @@ class SystemConfig:
     pieces_per_lane: int | None = None
     contract: bool | None = None
     chunk_group: int = 16
+    row_group: int | None = None
 
     def __post_init__(self):
         if self.precision not in matrixstore.PRECISIONS:
@@ -104,10 +111,20 @@ class SystemConfig:
             raise ValueError("contract=True changes rounding; it needs order='native'")
         if self.chunk_group < 1:
             raise ValueError("chunk_group must be >= 1")
+        if self.row_group not in (None, 1, 2, 4):
+            raise ValueError("row_group must be 1, 2 or 4")
+        if (self.row_group or 1) > 1 and (self.order != "native" or
+                                          self.precision not in ("single", "mixed")):
+            raise ValueError("row_group > 1 needs order='native' and single/mixed precision")
 
     @property
-    def contract_effective(self) -> bool:
-        return bool(self.contract) and self.precision == "single"
+    def row_group_effective(self) -> int:
+        """None = 4 for native single precision (measured 13-16% faster than
+        one row per lane set at c2, profiles/r01_probe_*), 1 otherwise (FP16
+        storage: one row per lane is fastest)."""
+        if self.row_group is not None:
+            return self.row_group
+        return 4 if self.order == "native" and self.precision == "single" else 1
 
 
 @dataclass
@@ -126,12 +143,15 @@ def configure_execution(sides, config) -> None:
     """Apply the config's kernel execution knobs to every staged block."""
     for side in sides:
         for blk in side.blocks:
-            matrixstore.set_execution(blk, config.contract_effective, config.chunk_group)
+            grouped = int(getattr(blk.info, "row_group", 1) or 1) > 1
+            c = grouped if config.contract is None else bool(config.contract)
+            matrixstore.set_execution(blk, c and config.order == "native", config.chunk_group)
 
 
-def _rows_per_warp(cfg) -> int:
+def _rows_per_warp(cfg, row_group: int | None = None) -> int:
     ppl = cfg.pieces_per_lane or 2
-    return 32 // matrixstore.lanes_for(cfg.ffactor, cfg.precision, ppl)
+    G = cfg.row_group_effective if row_group is None else row_group
+    return 32 // matrixstore.lanes_for(cfg.ffactor, cfg.precision, ppl) * G
 
 
 def _csr_host(matrix):
@@ -252,14 +272,18 @@ class AssembledSystem:
             if cfg.order == "reference" or g is None:
                 return matrixstore.reference_plan(ip, ix, n_rows, n_cols, cfg.block_partitions,
                                                   cfg.stage_capacity_bytes, cfg.ffactor,
-                                                  cfg.precision, rw, cfg.warps_per_cta)
-            plan = matrixstore.forward_plan(g.num_angles, g.grid_n, rw, cfg.warps_per_cta)
+                                                  cfg.precision, _rows_per_warp(cfg, 1),
+                                                  cfg.warps_per_cta)
+            plan = matrixstore.forward_plan(g.num_angles, g.grid_n, rw, cfg.warps_per_cta,
+                                            row_group=cfg.row_group_effective)
             return matrixstore.assign_forward_regimes(plan, g.angles, g.grid_n)
         # adjoint: every per-voxel order keyed by ascending ray id is the
         # reference order (src/matrixstore.py:189-201 sorts entries by ray)
         if g is not None and n_rows == g.num_voxels and n_cols == g.num_rays:
-            return matrixstore.adjoint_plan(g.num_angles, g.grid_n, rw, cfg.warps_per_cta)
-        return matrixstore.row_block_plan(n_rows, n_cols, rw, cfg.warps_per_cta)
+            return matrixstore.adjoint_plan(g.num_angles, g.grid_n, rw, cfg.warps_per_cta,
+                                            row_group=cfg.row_group_effective)
+        return matrixstore.row_block_plan(n_rows, n_cols, rw, cfg.warps_per_cta,
+                                          row_group=cfg.row_group_effective)
 
     def _budget(self, plan) -> int:
         return smem_budget_for(self.config, plan)
@@ -278,7 +302,7 @@ class AssembledSystem:
         cfg, g = self.config, self.geometry
         tomo, sino = hilbert_subdomains(g, cfg.tile_size, cfg.p_d)
         self.tomogram_subdomains, self.sinogram_subdomains = tomo, sino
-        rw = _rows_per_warp(cfg)
+        rw = _rows_per_warp(cfg, 1)
 
         def build(bip, bix, bv, nr, nc):
             plan = matrixstore.reference_plan(bip, bix, nr, nc, cfg.block_partitions,
@@ -549,11 +573,12 @@ class StreamedAssembly:
     def _forward(self, exp):
         cfg, g = self.cfg, self.g
         n = g.grid_n
-        ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta)
+        ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta, cfg.row_group_effective)
         parts = []
         tm = _Timer()
         for k0, k1 in self._chunks(ta):
-            plan = matrixstore.forward_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, k0, k1)
+            plan = matrixstore.forward_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, k0, k1,
+                                            row_group=cfg.row_group_effective)
             plan = matrixstore.assign_forward_regimes(plan, g.angles, n)
             base = k0 * n
             plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - base, -1).astype(np.int32)
@@ -578,7 +603,7 @@ class StreamedAssembly:
         import torch
         cfg, g = self.cfg, self.g
         n, R = g.grid_n, g.num_rays
-        tz = matrixstore.adjoint_tile_height(n, self.rw, cfg.warps_per_cta)
+        tz = matrixstore.adjoint_tile_height(n, self.rw, cfg.warps_per_cta, cfg.row_group_effective)
         per = max(1, int(self.BAND_NNZ // (1.2 * g.num_angles * n)))
         per = max(tz, per // tz * tz)
         st = _lib.stream_handle(self.dev)
@@ -625,7 +650,8 @@ class StreamedAssembly:
             t_ip, t_ix, t_v = _transpose(bip, bix, bv, R, hi - lo, alloc=self._buf)
             del bip, bix, bv
             tm.lap("transpose")
-            plan = matrixstore.adjoint_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, z0, z1)
+            plan = matrixstore.adjoint_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, z0, z1,
+                                            row_group=cfg.row_group_effective)
             plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - lo, -1).astype(np.int32)
             tm.lap("plan")
             hf = matrixstore.build_format(t_ip, t_ix, t_v, hi - lo, R, plan, cfg.precision,
@@ -644,7 +670,7 @@ class StreamedAssembly:
         import torch
         from .parallel import MatrixInfo
         cfg, g = self.cfg, self.g
-        ta = matrixstore.forward_tile_height(g.grid_n, self.rw, cfg.warps_per_cta)
+        ta = matrixstore.forward_tile_height(g.grid_n, self.rw, cfg.warps_per_cta, cfg.row_group_effective)
         chunks = self._chunks(ta)
         exp = self._exponent(chunks) if cfg.precision in ("half", "mixed") else 0
         self.nnz = 0

@@ -43,7 +43,8 @@ def export(ip, ix, v, n_rows, n_cols, plan, prec, ff, exp=0, budget=96 * 1024, s
     rec = f_dev * matrixstore.element_bytes(prec)
     cap = min(65536, budget // (2 * rec))
     lp = (rec // 16).bit_length() - 1
-    lg = (32 // plan.rows_per_warp).bit_length() - 1
+    G = plan.row_group
+    lg = (32 // (plan.rows_per_warp // G)).bit_length() - 1
     h = C.c_void_p()
     L = _lib.lib()
     rows = np.ascontiguousarray(plan.cta_rows, np.int32)
@@ -52,7 +53,7 @@ def export(ip, ix, v, n_rows, n_cols, plan, prec, ff, exp=0, budget=96 * 1024, s
                             np.ascontiguousarray(plan.key_tables, np.int32).ctypes.data,
                             np.ascontiguousarray(plan.cta_table, np.int32).ctypes.data, cap,
                             _lib.PREC_CODE[prec], exp, lp if schedule else -1,
-                            lg if schedule else -1, 4, C.byref(h))
+                            lg if schedule else -1, G, 4, C.byref(h))
     _lib.check(st, "build")
     info = _lib.FormatInfo()
     L.xct_format_get_info(h, C.byref(info))
@@ -62,7 +63,7 @@ def export(ip, ix, v, n_rows, n_cols, plan, prec, ff, exp=0, budget=96 * 1024, s
              so=np.empty(max(1, info.n_groups * w), np.int64),
              sw=np.empty(max(1, info.n_groups * w), np.int32),
              sl=np.empty(max(1, info.n_padded), np.uint16),
-             v=np.empty(max(1, info.n_padded), matrixstore.storage_dtype(prec)))
+             v=np.empty(max(1, info.n_padded * G), matrixstore.storage_dtype(prec)))
     L.xct_format_export(h, *[a[k].ctypes.data for k in ("gp", "mp", "m", "so", "sw", "sl", "v")])
     L.xct_format_free(h)
     return info, a, rows, cap
@@ -209,3 +210,97 @@ def test_bank_conflict_free_schedule(prec, side):
                     steps += 1
                     conflicts += len(pairs) - len({c for _, c in pairs})
     assert conflicts == 0, (conflicts, steps)
+
+
+def replay_grouped(info, a, rows, n_rows):
+    """Per-row (column, value) multisets of a row_group > 1 format: a unit of
+    G rows walks union entries holding one slot and G values."""
+    G = info.row_group
+    seqs = {r: [] for r in range(n_rows)}
+    rpw, w = info.rows_per_warp, info.warps_per_cta
+    upw = rpw // G
+    epp = 16 // info.value_bytes
+    for b in range(info.n_cta):
+        for g in range(a["gp"][b], a["gp"][b + 1]):
+            gmap = a["m"][a["mp"][g]:a["mp"][g + 1]]
+            for wi in range(w):
+                off, width = a["so"][g * w + wi], a["sw"][g * w + wi]
+                assert width % 4 == 0
+                for u in range(upw):
+                    for n in range(width):
+                        at = off + ((n // 4) * upw + u) * 4 + n % 4
+                        step0 = off + (n // 4) * upw * 4
+                        for gi in range(G):
+                            r = rows[b, (wi * upw + u) * G + gi]
+                            wd = (n % 4) * G + gi         # values [NV][units][16 B]
+                            val = a["v"][step0 * G + ((wd // epp) * upw + u) * epp + wd % epp]
+                            if r < 0:
+                                assert val == 0
+                            elif val != 0:
+                                seqs[r].append((int(gmap[a["sl"][at]]), float(val)))
+    return seqs
+
+
+@pytest.mark.parametrize("prec", ["single", "mixed"])
+@pytest.mark.parametrize("side", ["forward", "adjoint"])
+@pytest.mark.parametrize("G", [2, 4])
+def test_grouped_rows_format(prec, side, G):
+    """row_group G: every row's entries appear exactly once with its own
+    values (zeros elsewhere), the union is smaller than the sum of the rows,
+    and no two units of a quarter-warp read the same bank class in a step."""
+    g = O.make_geom(40, 1, 32)
+    A = O.system_matrix(g)
+    ip, ix, v = A.indptr, A.indices.astype(np.int32), A.values
+    n_rows, n_cols = A.num_rows, A.num_cols
+    rw = 32 // matrixstore.lanes_for(16, prec) * G
+    if side == "adjoint":
+        T = O.transpose_block(O.whole_block(A))
+        ip, ix, v = T.indptr, T.indices.astype(np.int32), T.values
+        n_rows, n_cols = n_cols, n_rows
+        plan = matrixstore.adjoint_plan(g.num_angles, g.n, rw, 4, row_group=G)
+    else:
+        plan = matrixstore.assign_forward_regimes(
+            matrixstore.forward_plan(g.num_angles, g.n, rw, 4, row_group=G), g.angles, g.n)
+    assert plan.row_group == G
+    covered = np.sort(plan.cta_rows[plan.cta_rows >= 0])
+    assert np.array_equal(covered, np.arange(n_rows))      # every row exactly once
+    info, a, rows, _ = export(ip, ix, v, n_rows, n_cols, plan, prec, 16, schedule=True)
+    assert info.row_group == G
+    seqs = replay_grouped(info, a, rows, n_rows)
+    sd = matrixstore.storage_dtype(prec)
+    for r in range(n_rows):
+        s_, e_ = ip[r], ip[r + 1]
+        want = sorted((int(c), float(sd(val))) for c, val in zip(ix[s_:e_], v[s_:e_]))
+        assert sorted(seqs[r]) == want, r
+    upw = info.rows_per_warp // G
+    L = 32 // upw
+    rq = max(1, 8 // L)
+    w = info.warps_per_cta
+    conflicts = 0
+    for gi in range(info.n_groups):
+        for wi in range(w):
+            off, width = a["so"][gi * w + wi], a["sw"][gi * w + wi]
+            if width == 0:
+                continue
+            sl = a["sl"][off:off + width * upw].reshape(width // 4, upw, 4)
+            sl = sl.transpose(0, 2, 1).reshape(width, upw).astype(np.int64)
+            cls = sl % rq
+            for q in range(upw // rq):
+                for n in range(width):
+                    pairs = set(zip(sl[n, q * rq:(q + 1) * rq].tolist(),
+                                    cls[n, q * rq:(q + 1) * rq].tolist()))
+                    conflicts += len(pairs) - len({c for _, c in pairs})
+    assert conflicts == 0
+
+
+def test_grouped_rows_repeated_column():
+    """A column repeated inside one row keeps its own union entry."""
+    ip = np.array([0, 3, 5, 7, 8], np.int64)
+    ix = np.array([0, 2, 0, 2, 1, 0, 0, 3], np.int32)
+    vals = np.array([1.0, 2.0, 3.0, 4.0, 5.0, 6.0, 7.0, 8.0])
+    plan = matrixstore.row_block_plan(4, 4, 64, 1, row_group=2)
+    info, a, rows, _ = export(ip, ix, vals, 4, 4, plan, "single", 16, schedule=True)
+    seqs = replay_grouped(info, a, rows, 4)
+    for r in range(4):
+        want = sorted((int(c), float(x)) for c, x in zip(ix[ip[r]:ip[r + 1]], vals[ip[r]:ip[r + 1]]))
+        assert sorted(seqs[r]) == want

@@ -304,3 +304,63 @@ def test_streamed_build_is_identical_to_monolithic(prec, monkeypatch):
     ref = solver.cgls_solve(mono, y.astype(np.float64), solver.SolveConfig(max_iters=3,
                                                                            precision=prec))
     assert np.array_equal(res.x, ref.x)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_grouped_rows_operator(G):
+    """row_group G (a lane set walks the union of G rows' entries): the
+    native-order tolerances of test_operator_application_g64, with and
+    without FFMA contraction, at F = 4 and 16."""
+    gold = load_golden("pipeline_g64")
+    g = geometry.make_geometry(96, 1, 64)
+    x, y = gold["x64"].astype(np.float32), gold["y64"]
+    for prec in ("single", "mixed"):
+        for ff in (4, 16):
+            for contract in ((False, True) if prec == "single" else (False,)):
+                sysm = pipeline.assemble(g, pipeline.SystemConfig(
+                    precision=prec, ffactor=ff, row_group=G, contract=contract))
+                assert sysm.forward.blocks[0].info.row_group == G
+                f, st = sysm.apply_forward(x)
+                a, _ = sysm.apply_adjoint(y)
+                gf, ga = gold[f"g64_fwd_{prec}_f{ff}"], gold[f"g64_adj_{prec}_f{ff}"]
+                assert np.array_equal([s.factor for s in st], gold[f"g64_fwdfac_{prec}_f{ff}"])
+                for out, ref in ((f, gf), (a, ga)):
+                    if prec == "single":
+                        assert rel_l2(out, ref) <= 1e-6, (ff, contract)
+                    else:
+                        assert rel_l2(out, ref) <= 1e-3
+                        assert np.mean(out != ref) <= 1e-2
+
+
+def test_grouped_rows_c1_cgls_and_streamed_build(monkeypatch):
+    """row_group 4 CGLS at c1 stays within twice the reference's own
+    order-noise floor; the streamed build of a grouped operator is
+    bit-identical to the monolithic one."""
+    import json
+    from conftest import GOLDEN
+    floor = json.loads((GOLDEN / "noise_floor.json").read_text())
+    gold = load_golden("c1")
+    g = geometry.make_geometry(180, 16, 128)
+    og = O.make_geom(180, 16, 128)
+    y = O.measure(O.system_matrix(og), O.phantom("shepp-logan-like", 128, 16))
+    for prec in ("single", "mixed"):
+        sysm = pipeline.assemble(g, pipeline.SystemConfig(precision=prec, ffactor=16,
+                                                           row_group=4))
+        res = solver.cgls_solve(sysm, y, solver.SolveConfig(max_iters=30, precision=prec))
+        curve = gold[f"cg_{prec}_residual"]
+        assert np.max(np.abs(np.array(res.residual_history) / curve - 1)) <= \
+            2 * max(floor[prec]["curve_max_rel"])
+        assert rel_l2(res.x, gold[f"cg_{prec}_x"]) <= 2 * max(floor[prec]["x_rel_l2"])
+    g = geometry.make_geometry(200, 8, 128)
+    monkeypatch.setattr(pipeline.StreamedAssembly, "CHUNK_NNZ", 6e5)
+    monkeypatch.setattr(pipeline.StreamedAssembly, "BAND_NNZ", 1e6)
+    rng = np.random.default_rng(3)
+    x = rng.random((g.num_voxels, 8)).astype(np.float32)
+    yv = rng.random((g.num_rays, 8)).astype(np.float32)
+    for prec in ("single", "mixed"):
+        st = pipeline.assemble(g, pipeline.SystemConfig(precision=prec, build="streamed",
+                                                         row_group=4))
+        mono = pipeline.assemble(g, pipeline.SystemConfig(precision=prec, build="monolithic",
+                                                           row_group=4))
+        assert np.array_equal(st.apply_forward(x)[0], mono.apply_forward(x)[0])
+        assert np.array_equal(st.apply_adjoint(yv)[0], mono.apply_adjoint(yv)[0])

@@ -32,7 +32,8 @@ def main():
     ap.add_argument("--slices", type=int, default=None)
     ap.add_argument("--order", default="native")
     ap.add_argument("--ppl", type=int, default=None)
-    ap.add_argument("--groups", default="1", help="chunk_group values to sweep")
+    ap.add_argument("--groups", default="16", help="chunk_group values to sweep")
+    ap.add_argument("--row-group", type=int, default=None)
     ap.add_argument("--contract", default="auto", help="auto | 0 | 1 | sweep")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -46,7 +47,7 @@ def main():
     t0 = time.perf_counter()
     system = pipeline.assemble(g, pipeline.SystemConfig(
         precision=cfg["precision"], ffactor=16, order=args.order, warps_per_cta=args.warps,
-        smem_budget=args.smem, pieces_per_lane=args.ppl))
+        smem_budget=args.smem, pieces_per_lane=args.ppl, row_group=args.row_group))
     t_asm = time.perf_counter() - t0
     nnz = system.matrix.nnz
     geometry.clear_matrix_cache()
@@ -56,6 +57,7 @@ def main():
     od = torch.float64 if prec == "double" else torch.float32
     eb = matrixstore.element_bytes(prec)
     out = {"config": args.config, "precision": prec, "slices": S, "nnz": nnz,
+           "row_group": args.row_group,
            "assemble_s": t_asm, "warps": args.warps, "smem": args.smem, "ppl": args.ppl}
     for name, side in (("forward", system.forward), ("adjoint", system.adjoint)):
         blk = side.blocks[0]
