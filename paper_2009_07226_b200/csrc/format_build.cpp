@@ -222,9 +222,8 @@ namespace {
 // ordered by (key, column) -- ascending ray id per voxel for the back
 // projection -- then placed on slab steps by the bank schedule.
 // Slab layout per (group, warp): slots [width/4][units_per_warp][4] (as for
-// G = 1) and values [width/4][NV][units_per_warp][16 B], NV = 4*G*vbytes/16:
-// 16-byte piece k of a unit holds its value words k*epp.., word = entry*G +
-// row, so every 128-bit value load of a warp reads one contiguous run.
+// G = 1) and values [width/4][units_per_warp][4][G]: a unit's step is one
+// contiguous run of 4*G values (NV 16-byte pieces at immediate offsets).
 struct UEnt {
   int32_t key, col, dup, slot;
   int64_t j[4];
@@ -487,19 +486,12 @@ int build_grouped(int64_t n_rows, int64_t n_cols, const int64_t* indptr, const i
       const int64_t at = F->slab_off[gg * warps + w] + ((n >> 2) * upw + uin) * 4 + (n & 3);
       F->slots[at] = (uint16_t)slot;
       if (!E) return;                          // padding: values stay 0
-      // values of a step: [NV][units][16 B]; piece k of a unit holds its
-      // words k*epp .. k*epp+epp-1, word = entry*G + row (so each 128-bit
-      // load instruction of a warp reads one contiguous run)
-      const int64_t epp = 16 / vbytes;
-      const int64_t step0 = F->slab_off[gg * warps + w] + (n >> 2) * upw * 4;
       for (int gi = 0; gi < G; ++gi) {
         const int64_t j = E->j[gi];
         if (j < 0) continue;
         const double v = values[j] * scale;
         double back;
-        const int64_t wd = (n & 3) * G + gi;
-        const int64_t vi = step0 * G + ((wd / epp) * upw + uin) * epp + wd % epp;
-        uint8_t* dst = F->values.get() + vi * vbytes;
+        uint8_t* dst = F->values.get() + (at * G + gi) * vbytes;
         if (precision == XCT_SINGLE) {
           float f = (float)v;
           std::memcpy(dst, &f, 4);

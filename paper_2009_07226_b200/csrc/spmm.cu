@@ -500,14 +500,11 @@ template <int G> struct GStep<XCT_SINGLE, G> {
   static constexpr int NV = G;                      // 4 entries * G * 4 B / 16
   uint2 s;
   uint4 v[NV];
-  // vb: 16-byte piece index of this unit's first value piece in the step;
-  // piece k sits upw pieces further (values [NV][units][16 B] per step)
-  __device__ void load(const uint16_t* sl, const void* vv, int64_t idx, int64_t vb, int upw,
-                       uint64_t pol) {
-    s = ld_stream_u2(sl + idx, pol);
-    const uint4* pv = reinterpret_cast<const uint4*>(vv) + vb;
+  // sp: this unit's 4 slots of the step; vp: its NV value pieces
+  __device__ void load(const uint16_t* sp, const uint4* vp, uint64_t pol) {
+    s = ld_stream_u2(sp, pol);
 #pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = ld_stream_u4(pv + (int64_t)k * upw, pol);
+    for (int k = 0; k < NV; ++k) v[k] = ld_stream_u4(vp + k, pol);
   }
   __device__ uint32_t off(int e) const {
     uint32_t q = e < 2 ? s.x : s.y;
@@ -524,14 +521,11 @@ template <int G> struct GStep<XCT_MIXED, G> {
   static constexpr int NV = G / 2;                  // 4 entries * G * 2 B / 16
   uint2 s;
   uint4 v[NV];
-  // vb: 16-byte piece index of this unit's first value piece in the step;
-  // piece k sits upw pieces further (values [NV][units][16 B] per step)
-  __device__ void load(const uint16_t* sl, const void* vv, int64_t idx, int64_t vb, int upw,
-                       uint64_t pol) {
-    s = ld_stream_u2(sl + idx, pol);
-    const uint4* pv = reinterpret_cast<const uint4*>(vv) + vb;
+  // sp: this unit's 4 slots of the step; vp: its NV value pieces
+  __device__ void load(const uint16_t* sp, const uint4* vp, uint64_t pol) {
+    s = ld_stream_u2(sp, pol);
 #pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = ld_stream_u4(pv + (int64_t)k * upw, pol);
+    for (int k = 0; k < NV; ++k) v[k] = ld_stream_u4(vp + k, pol);
   }
   __device__ uint32_t off(int e) const {
     uint32_t q = e < 2 ? s.x : s.y;
@@ -596,18 +590,23 @@ __global__ void __launch_bounds__(512) spmm_grouped_kernel(const Params p) {
   const int64_t step = (int64_t)upw * 4;
   int64_t at = (g0 < g1 ? p.slab_off[(int64_t)g0 * p.warps_per_cta + warp] : 0) +
                (int64_t)uin * 4;
-  // value pieces: a step of the warp is NV*upw pieces; this unit's first
-  // piece of the step starting at position s0 (= at - 4*uin) is s0/4*NV + uin
-  const int64_t vstep = (int64_t)St::NV * upw;
-  int64_t vb = (at - 4 * uin) / 4 * St::NV + uin;
   constexpr int D = RingDepth<PREC, NPL, G>::value;
   // The warp's steps of all groups form one stream: r[i] holds the steps
   // k = i mod D, and the load of step k + D is issued as soon as step k is
   // consumed, straight through group boundaries (one copy of the unrolled
   // body -- phase-specialised copies overflow the instruction cache).
+  // Load pointers run D steps ahead: slots + position, values + position/4
+  // * NV pieces (a unit's step = NV contiguous pieces).
+  const uint16_t* lsp = p.slots + at;
+  const uint4* lvp = reinterpret_cast<const uint4*>(p.values) + at / 4 * St::NV;
+  const int64_t vstep = (int64_t)St::NV * upw;
   St r[D];
 #pragma unroll
-  for (int i = 0; i < D; ++i) r[i].load(p.slots, p.values, at + i * step, vb + i * vstep, upw, pol_e);
+  for (int i = 0; i < D; ++i) {
+    r[i].load(lsp, lvp, pol_e);
+    lsp += step;
+    lvp += vstep;
+  }
   int32_t* const maps = reinterpret_cast<int32_t*>(
       reinterpret_cast<char*>(stage) + 2 * (size_t)bb);
   int32_t* const map0 = maps;
@@ -653,9 +652,9 @@ __global__ void __launch_bounds__(512) spmm_grouped_kernel(const Params p) {
         enter(g);
       }
       consume_g<NPL, G>(acc, r[i], pb);
-      r[i].load(p.slots, p.values, at + D * step, vb + D * vstep, upw, pol_e);
-      at += step;
-      vb += vstep;
+      r[i].load(lsp, lvp, pol_e);
+      lsp += step;
+      lvp += vstep;
       --left;
     }
   }
