@@ -1,5 +1,3 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k grouped > gpurun_out/pytest_grouped.log 2>&1; echo pytest=$? 
-P="python tools/spmm_probe.py --reps 3"
-$P --config c2 > gpurun_out/t_c2_g4.json 2>gpurun_out/t.err
-$P --config c2m --row-group 2 --ppl 2 > gpurun_out/t_c2m_g2_l1.json 2>>gpurun_out/t.err
-tail -3 gpurun_out/t.err
+TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512"
+XCT_VERBOSE=1 timeout 2400 $TR bench.py --gpus 4 --config c5 --partition domain --no-cpu-baseline --no-e2e --steps 5 --warmup 3 > gpurun_out/bench_c5_dom4.log 2>&1; echo dom4=$?
+grep metric gpurun_out/bench_c5_dom4.log | cut -c1-600
