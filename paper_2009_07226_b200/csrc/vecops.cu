@@ -462,7 +462,8 @@ __global__ void scale_chunks_k(T* v, int64_t per_chunk, int64_t n_chunks, const 
 
 extern "C" int xct_gather_rows(const void* d_src, int64_t n_src, const int32_t* d_idx, int64_t m,
                                int64_t n_chunks, int32_t fd, int f64, void* d_dst, void* stream) {
-  if (!d_src || !d_dst || (m && !d_idx)) return xct::fail(XCT_EINVAL, "gather_rows: bad argument");
+  if (m == 0 || n_chunks == 0 || fd == 0) return XCT_OK;     // empty exchange list
+  if (!d_src || !d_dst || !d_idx) return xct::fail(XCT_EINVAL, "gather_rows: bad argument");
   const int64_t total = n_chunks * m * fd;
   if (total == 0) return XCT_OK;
   cudaStream_t s = (cudaStream_t)stream;
@@ -475,7 +476,8 @@ extern "C" int xct_gather_rows(const void* d_src, int64_t n_src, const int32_t* 
 extern "C" int xct_accumulate_rows(void* d_dst, int64_t n_dst, const void* d_src,
                                    const int32_t* d_pos, int64_t m, int64_t n_chunks, int32_t fd,
                                    int f64, void* stream) {
-  if (!d_src || !d_dst || (m && !d_pos)) return xct::fail(XCT_EINVAL, "accumulate_rows: bad argument");
+  if (m == 0 || n_chunks == 0 || fd == 0) return XCT_OK;     // empty exchange list
+  if (!d_src || !d_dst || !d_pos) return xct::fail(XCT_EINVAL, "accumulate_rows: bad argument");
   const int64_t total = n_chunks * m * fd;
   if (total == 0) return XCT_OK;
   cudaStream_t s = (cudaStream_t)stream;
@@ -488,7 +490,8 @@ extern "C" int xct_accumulate_rows(void* d_dst, int64_t n_dst, const void* d_src
 extern "C" int xct_scale_chunks(void* d_v, int64_t per_chunk, int64_t n_chunks,
                                 const double* d_factors, int f64, double* d_scratch,
                                 double* d_sumsq, void* stream) {
-  if (!d_v || !d_factors) return xct::fail(XCT_EINVAL, "scale_chunks: bad argument");
+  if ((!d_v && n_chunks * per_chunk) || !d_factors)
+    return xct::fail(XCT_EINVAL, "scale_chunks: bad argument");
   const int64_t total = n_chunks * per_chunk;
   cudaStream_t s = (cudaStream_t)stream;
   if (total == 0) {

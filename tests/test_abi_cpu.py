@@ -301,3 +301,13 @@ def test_grouped_rows_repeated_column():
     for r in range(4):
         want = sorted((int(c), float(x)) for c, x in zip(ix[ip[r]:ip[r + 1]], vals[ip[r]:ip[r + 1]]))
         assert sorted(seqs[r]) == want
+
+
+def test_exchange_kernels_accept_empty_lists():
+    """A rank whose footprint shares nothing with a peer (or with itself)
+    has empty K10 lists: gather/accumulate of zero rows is a no-op, even
+    with the NULL data pointer of an empty tensor (no CUDA call is made)."""
+    L = _lib.lib()
+    assert L.xct_gather_rows(None, 0, None, 0, 16, 16, 0, None, None) == 0
+    assert L.xct_accumulate_rows(None, 0, None, None, 0, 16, 16, 0, None) == 0
+    assert L.xct_gather_rows(None, 10, None, 5, 16, 16, 0, None, None) != 0
