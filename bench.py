@@ -198,14 +198,17 @@ def _global_nnz(system):
 
 
 def metric_name(cfg):
-    return (f"SpMM GFLOPS & CG s/iter ({cfg['n']}^2 x {cfg['slices']} slices/GPU, "
+    per = "slices" if cfg.get("strong") else "slices/GPU"
+    return (f"SpMM GFLOPS & CG s/iter ({cfg['n']}^2 x {cfg['slices']} {per}, "
             f"{cfg['k']} angles, {cfg['precision']})")
 
 
 def config_block(cfg, ws):
     total = cfg["slices"] if cfg.get("strong") else cfg["slices"] * ws
     return {"workload": cfg["desc"], "n": cfg["n"], "angles": cfg["k"],
-            "slices_per_gpu": cfg["slices"] if not cfg.get("strong") else -(-total // ws),
+            # domain partition: every GPU holds all slices of its image/sinogram tiles
+            "slices_per_gpu": (cfg["slices"] if not cfg.get("strong") or cfg.get("domain")
+                               else -(-total // ws)),
             "total_slices": total,
             "precision": cfg["precision"], "ffactor": 16, "step": "one CGLS iteration",
             "parallelism": (f"image-domain P_d={ws}" if cfg.get("domain") else

@@ -323,6 +323,7 @@ class CGLSRun:
         # streamed one slice chunk at a time
         is_host = isinstance(y, np.ndarray) or not y.is_cuda
         nbytes = n_rows * S * 8
+        lap = _Lap(cg.dev)
         if is_host and nbytes <= min(16 << 30, torch.cuda.mem_get_info(cg.dev)[0] // 4):
             yd = torch.empty((n_rows, S), dtype=torch.float64, device=cg.dev)
             rows_per = max(1, (256 << 20) // max(1, S * 8))
@@ -333,6 +334,7 @@ class CGLSRun:
                     blk = torch.from_numpy(np.ascontiguousarray(blk, dtype=np.float64))
                 yd[r0:r1].copy_(blk, non_blocking=True)
             y, owned = yd, None
+            lap("start: upload y")
 
         def chunk(c):
             lo, hi = c * cg.F, min(S, (c + 1) * cg.F)
@@ -361,6 +363,7 @@ class CGLSRun:
                       dst.data_ptr(), cg.st)
             if cg.reduced:
                 _lib.call("xct_maxabs", tmp.data_ptr(), 1, per, 1.0, rbits.data_ptr(), cg.st)
+        lap("start: y norm and store pass 1")
         cg.comm.max_bits(ybits)
         if not math.isfinite(float(ybits.cpu().numpy().view(np.float64)[0])):
             raise SolverDivergence(0, prec, "measurement data contains NaN or Inf")
@@ -393,7 +396,9 @@ class CGLSRun:
         buf = torch.empty(cg.numel(max(n_rows, n_cols)), dtype=cg.out_dt, device=cg.dev)
         self.s_buf = buf[:cg.numel(n_cols)]
         self.q_buf = buf[:cg.numel(n_rows)]
+        lap("start: store pass 2")
         facs, gamma = cg.apply(system.adjoint, self.r, self.s_buf)
+        lap("start: first back projection")
         if facs is None:
             raise SolverDivergence(0, prec, "residual contains NaN or Inf")
         self.result.backprojections += 1
@@ -463,6 +468,7 @@ class CGLSRun:
             if not self.is_np:
                 out = torch.zeros((n_cols, S), dtype=torch.float64, device=cg.dev)
         else:
+            lap = _Lap(cg.dev)
             xf = torch.empty((n_cols, S), dtype=torch.float64, device=cg.dev)
             _lib.call("xct_unchunk_f64", self.x.t.data_ptr(), self.x.code,
                       float(np.float32(self.x.factor)), n_cols, S, cg.F, cg.f_dev,
@@ -473,8 +479,30 @@ class CGLSRun:
                 out = xf.cpu()
             else:
                 out = xf
+            lap("finish: x to the caller")
         self.result.x = out[:, 0] if self.squeeze else out
         return self.result
+
+
+class _Lap:
+    """Phase timer of the solve's host-facing steps (XCT_VERBOSE only: it
+    synchronizes the device)."""
+
+    def __init__(self, dev):
+        import os
+        self.on = bool(os.environ.get("XCT_VERBOSE"))
+        self.dev = dev
+        self.t = time.perf_counter()
+
+    def __call__(self, what):
+        if not self.on:
+            return
+        import sys
+        import torch
+        torch.cuda.synchronize(self.dev)
+        now = time.perf_counter()
+        print(f"[xct] cgls {what} {now - self.t:.3f} s", file=sys.stderr, flush=True)
+        self.t = now
 
 
 def cgls_solve(system, y, config: SolveConfig) -> SolveResult:
