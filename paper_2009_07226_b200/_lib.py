@@ -190,7 +190,9 @@ def to_host(t, out: np.ndarray | None = None) -> np.ndarray:
         out.reshape(-1).view(np.uint8)[:] = t.reshape(-1).view(torch.uint8).numpy()
         return out
     src = t.reshape(-1).view(torch.uint8)
-    dst = out.reshape(-1).view(np.uint8)
+    # host-side copies with torch (multi-threaded: the first touch of a
+    # fresh result array is what a pageable .cpu() pays for, ~1 s per 2 GB)
+    dst = torch.from_numpy(out.reshape(-1).view(np.uint8))
     bufs, views, evs = _staging(t.device)
     blocks = [(b, min(n, b + _STAGE_BYTES)) for b in range(0, n, _STAGE_BYTES)]
     for i, (b0, b1) in enumerate(blocks):
@@ -199,10 +201,10 @@ def to_host(t, out: np.ndarray | None = None) -> np.ndarray:
         if i:
             p0, p1 = blocks[i - 1]
             evs[(i - 1) & 1].synchronize()
-            dst[p0:p1] = views[(i - 1) & 1][:p1 - p0]
+            dst[p0:p1].copy_(bufs[(i - 1) & 1][:p1 - p0])
     p0, p1 = blocks[-1]
     evs[(len(blocks) - 1) & 1].synchronize()
-    dst[p0:p1] = views[(len(blocks) - 1) & 1][:p1 - p0]
+    dst[p0:p1].copy_(bufs[(len(blocks) - 1) & 1][:p1 - p0])
     return out
 
 

@@ -261,15 +261,18 @@ constexpr int kFillUnroll = 4;
 // Stage the records of load group g into the buffer at shared address dst,
 // reading the group's slot->element map from shared memory (it was copied
 // there one group earlier, so no dependent global load sits on this path).
+// blockDim is a multiple of the NP pieces of a record, so a thread always
+// copies the same piece q: its plane offset and source offset are loop
+// invariant, and the loop is one LDS + one address IMAD + one LDGSTS.
 __device__ __forceinline__ void stage_fill(const Params& p, const uint4* xb, uint32_t dst,
                                            const int32_t* map, int ns, int lp, uint64_t pol) {
-  const int pieces = ns << lp;
-  const int NP = 1 << lp;
-  for (int i = threadIdx.x; i < pieces; i += blockDim.x) {
-    const int s = i >> lp, q = i & (NP - 1);
-    cp_async16(dst + plane_base(q, lp, p.plane_slots) + ((uint32_t)s << 4),
-               xb + ((int64_t)map[s] << lp) + q, pol);
-  }
+  const int q = threadIdx.x & ((1 << lp) - 1);
+  const uint32_t dq = dst + plane_base(q, lp, p.plane_slots);
+  const uint4* xq = xb + q;
+  const int sstep = blockDim.x >> lp;
+#pragma unroll 1
+  for (int s = threadIdx.x >> lp; s < ns; s += sstep)
+    cp_async16(dq + ((uint32_t)s << 4), xq + ((uint32_t)map[s] << lp), pol);
 }
 
 // Copy the slot->element map of group g into shared memory (4-byte cp.async).

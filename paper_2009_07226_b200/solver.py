@@ -473,10 +473,13 @@ class CGLSRun:
             _lib.call("xct_unchunk_f64", self.x.t.data_ptr(), self.x.code,
                       float(np.float32(self.x.factor)), n_cols, S, cg.F, cg.f_dev,
                       xf.data_ptr(), cg.st)
-            if self.is_np:
-                out = xf.cpu().numpy()
-            elif not self.y.is_cuda:          # host tensor in -> host tensor out
-                out = xf.cpu()
+            if self.is_np or not self.y.is_cuda:
+                # host in -> host out, through pinned staging (a pageable
+                # .cpu() of a 2 GB result takes ~1 s on the B200 host)
+                torch.cuda.synchronize(cg.dev)
+                out = _lib.to_host(xf)
+                if not self.is_np:
+                    out = torch.from_numpy(out)
             else:
                 out = xf
             lap("finish: x to the caller")
