@@ -356,10 +356,13 @@ def main():
         return blk.nnz * b_e * n_chunks + (blk.n_in + blk.n_out) * S * b_x
     bytes_fwd, bytes_adj = side_bytes(system.forward), side_bytes(system.adjoint)
     bytes_app = (bytes_fwd + bytes_adj) / 2
-    spmm_ms = [a.elapsed_time(b) for _, a, b in events]
+    # events: (forward?, start, end[, fraction of the application]) -- the
+    # domain-partitioned operator launches K6 in F-chunk waves
+    spmm_ms = [e[1].elapsed_time(e[2]) for e in events]
     t_spmm = sum(spmm_ms) / 1e3
-    n_spmm = len(spmm_ms)
-    moved = sum(bytes_fwd if fw else bytes_adj for fw, _, _ in events)
+    frac = [e[3] if len(e) > 3 else 1.0 for e in events]
+    n_spmm = sum(frac)
+    moved = sum((bytes_fwd if e[0] else bytes_adj) * f for e, f in zip(events, frac))
     achieved = moved / t_spmm / 1e9 if t_spmm > 0 else 0.0
     peak, peak_src = hbm_peak()
     local_nnz = (system.forward.blocks[0].nnz + system.adjoint.blocks[0].nnz) / 2

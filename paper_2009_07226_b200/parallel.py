@@ -148,47 +148,67 @@ class _DistSide:
                 self.recv[s] = t(np.searchsorted(own_ids, hit))
         del owner
 
+    # F-chunk waves per application: the exchange of wave w (gather, NCCL
+    # p2p over NVLink) runs on NCCL's stream while K6 computes wave w + 1
+    WAVES = 4
+
     def exchange_apply(self, cg, xin, out, fac) -> float:
         """Local partial SpMM, exchange, reduction in the reference's direct
         plan order (owner first, then senders ascending), denormalize.
-        Returns the local sum of squares of the owned outputs."""
+        The F-chunks go in waves so each wave's exchange overlaps the next
+        wave's SpMM; every output element still sums the same partials in
+        the same order.  Returns the local sum of squares of the owned
+        outputs."""
         import torch
         import torch.distributed as dist
         from . import _lib, engine
         C, fd = cg.n_chunks, cg.f_dev
         f64 = int(cg.out_dt == torch.float64)
         partial = torch.empty((C, self.n_fp, fd), dtype=cg.out_dt, device=cg.dev)
-        ev = cg.events
-        if ev is not None:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-        engine.apply_side(self.block, xin, partial, row_stride=fd, chunk_stride=self.n_fp * fd,
-                          valid_cols=C * fd, ffactor_out=fd, factors=None, stream=cg.st)
-        if ev is not None:
-            e1.record()
-            ev.append((self is cg.sys.forward, e0, e1))
-
-        def gather(idx):
-            buf = torch.empty((C, idx.numel(), fd), dtype=cg.out_dt, device=cg.dev)
-            _lib.call("xct_gather_rows", partial.data_ptr(), self.n_fp, idx.data_ptr(),
-                      idx.numel(), C, fd, f64, buf.data_ptr(), cg.st)
-            return buf
-        sends = {q: gather(idx) for q, idx in self.send.items()}
-        recvs = {s: torch.empty((C, idx.numel(), fd), dtype=cg.out_dt, device=cg.dev)
-                 for s, idx in self.recv.items()}
-        ops = [dist.P2POp(dist.isend, b, q) for q, b in sends.items()]
-        ops += [dist.P2POp(dist.irecv, b, s) for s, b in recvs.items()]
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
         o = out.view(C, self.num_outputs, fd)
-        o.zero_()
-        own = gather(self.self_src)
-        _lib.call("xct_accumulate_rows", o.data_ptr(), self.num_outputs, own.data_ptr(),
-                  self.self_dst.data_ptr(), self.self_dst.numel(), C, fd, f64, cg.st)
-        for s in sorted(recvs):
-            _lib.call("xct_accumulate_rows", o.data_ptr(), self.num_outputs, recvs[s].data_ptr(),
-                      self.recv[s].data_ptr(), self.recv[s].numel(), C, fd, f64, cg.st)
+        W = max(1, min(self.WAVES, C))
+        bounds = [(C * w // W, C * (w + 1) // W) for w in range(W)]
+        bounds = [(a, b) for a, b in bounds if b > a]
+        ev = cg.events
+
+        def gather(idx, c0, c1):
+            buf = torch.empty((c1 - c0, idx.numel(), fd), dtype=cg.out_dt, device=cg.dev)
+            _lib.call("xct_gather_rows", partial[c0:c1].data_ptr(), self.n_fp, idx.data_ptr(),
+                      idx.numel(), c1 - c0, fd, f64, buf.data_ptr(), cg.st)
+            return buf
+
+        pending = []
+        for c0, c1 in bounds:
+            if ev is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            engine.apply_side(self.block, xin[c0:c1], partial[c0:c1], row_stride=fd,
+                              chunk_stride=self.n_fp * fd, valid_cols=(c1 - c0) * fd,
+                              ffactor_out=fd, factors=None, stream=cg.st)
+            if ev is not None:
+                e1.record()
+                ev.append((self is cg.sys.forward, e0, e1, (c1 - c0) / C))
+            sends = {q: gather(idx, c0, c1) for q, idx in self.send.items()}
+            recvs = {s: torch.empty((c1 - c0, idx.numel(), fd), dtype=cg.out_dt,
+                                    device=cg.dev)
+                     for s, idx in self.recv.items()}
+            ops = [dist.P2POp(dist.isend, b, q) for q, b in sends.items()]
+            ops += [dist.P2POp(dist.irecv, b, s) for s, b in recvs.items()]
+            works = dist.batch_isend_irecv(ops) if ops else []
+            pending.append((c0, c1, works, sends, recvs))
+        for c0, c1, works, sends, recvs in pending:
+            ow = o[c0:c1]
+            ow.zero_()
+            own = gather(self.self_src, c0, c1)
+            _lib.call("xct_accumulate_rows", ow.data_ptr(), self.num_outputs, own.data_ptr(),
+                      self.self_dst.data_ptr(), self.self_dst.numel(), c1 - c0, fd, f64, cg.st)
+            for r in works:
+                r.wait()            # the current stream waits for NCCL; the host does not
+            for s in sorted(recvs):
+                _lib.call("xct_accumulate_rows", ow.data_ptr(), self.num_outputs,
+                          recvs[s].data_ptr(), self.recv[s].data_ptr(), self.recv[s].numel(),
+                          c1 - c0, fd, f64, cg.st)
         _lib.call("xct_scale_chunks", o.data_ptr(), self.num_outputs * fd, C, fac.data_ptr(), f64,
                   cg.scratch.data_ptr(), cg.scal.data_ptr(), cg.st)
         return float(cg.scal[0].item())

@@ -8,6 +8,7 @@ import subprocess
 import sys
 from pathlib import Path
 
+import numpy as np
 import xct_oracle as O
 from paper_2009_07226_b200 import parallel
 
@@ -39,3 +40,57 @@ def test_broadcast_side_gloo_world2(tmp_path):
     for k in ("digest", "nnz", "smem", "groups"):
         assert r0[k] == r1[k], k
     assert r0["nnz"] > 0 and r0["groups"] > 0
+
+
+def _csr_apply(ip, ix, v, x):
+    rows = np.repeat(np.arange(len(ip) - 1), np.diff(ip))
+    out = np.zeros((len(ip) - 1,) + x.shape[1:])
+    np.add.at(out, rows, v[:, None] * x[ix])
+    return out
+
+
+def test_domain_exchange_plan_reassembles_the_operator():
+    """Host logic of the P_d > 1 exchange (parallel._DistSide): each rank
+    multiplies its column block, then the send / recv / self maps route
+    every partial to the owner of its output element.  Emulating the NCCL
+    p2p with array copies, the owners' sums reproduce A x and A^T y."""
+    from paper_2009_07226_b200 import geometry, pipeline
+    g = geometry.make_geometry(40, 1, 24)
+    og = O.make_geom(40, 1, 24)
+    A = O.system_matrix(og)
+    ip, ix, v = A.indptr, A.indices.astype(np.int32), A.values
+    R, Cn = A.num_rows, A.num_cols
+    P = 3
+    tomo, sino = pipeline.hilbert_subdomains(g, 8, P)
+    rng = np.random.default_rng(0)
+    x = rng.random((Cn, 2))
+    y = rng.random((R, 2))
+    for direction in ("forward", "adjoint"):
+        blocks, fps = [], []
+        for r in range(P):
+            if direction == "forward":
+                bip, bix, bv, fp = pipeline.column_block(ip, ix, v, R, Cn, tomo[r].elements)
+                blocks.append(_csr_apply(bip, bix, bv, x[tomo[r].elements]))
+            else:
+                bip, bix, bv, fp = pipeline.row_block_transposed(ip, ix, v, sino[r].elements)
+                blocks.append(_csr_apply(bip, bix, bv, y[sino[r].elements]))
+            fps.append(fp)
+        owned = [s.elements for s in (sino if direction == "forward" else tomo)]
+        ins = [s.elements for s in (tomo if direction == "forward" else sino)]
+        sides = [parallel._DistSide(None, fps[r], owned[r], ins[r], fps, owned, r, "cpu")
+                 for r in range(P)]
+        full = (_csr_apply(ip, ix, v, x) if direction == "forward"
+                else _csr_apply(*O_transpose(ip, ix, v, R, Cn), y))
+        for q in range(P):
+            me = sides[q]
+            acc = np.zeros((len(owned[q]), 2))
+            acc[me.self_dst.numpy()] += blocks[q][me.self_src.numpy()]
+            for s in sorted(me.recv):
+                sent = blocks[s][sides[s].send[q].numpy()]
+                acc[me.recv[s].numpy()] += sent
+            assert np.allclose(acc, full[owned[q]], rtol=1e-12, atol=1e-12), (direction, q)
+
+
+def O_transpose(ip, ix, v, n_rows, n_cols):
+    from paper_2009_07226_b200.pipeline import _transpose
+    return _transpose(ip, ix, v, n_rows, n_cols)
