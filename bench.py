@@ -369,7 +369,7 @@ def main():
     spmm_gflops = 2.0 * local_nnz * S * n_spmm / t_spmm / 1e9 if t_spmm > 0 else 0.0
     traffic = None
     tf = ROOT / "profiles" / f"traffic_{args.config}_{cfg['precision']}.json"
-    if tf.exists():
+    if tf.exists() and ws == 1:     # the ncu capture is of the one-GPU launch
         traffic = json.loads(tf.read_text()).get("bytes_per_launch")
 
     # end to end through the public API: host y in (pinned), host x out

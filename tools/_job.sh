@@ -1,3 +1,3 @@
-XCT_VERBOSE=1 timeout 900 python bench.py > gpurun_out/bench_c2_v14.log 2>&1; echo b=$?
-python tools/spmm_probe.py --reps 3 --config c2m > gpurun_out/v_c2m_g1.json 2>gpurun_out/v.err
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512"
+timeout 2400 $TR bench.py --gpus 4 --config c5 --partition domain --no-cpu-baseline --no-e2e --steps 5 --warmup 3 > gpurun_out/bench_c5_dom4_w.log 2>&1; echo dom4=$?
+grep metric gpurun_out/bench_c5_dom4_w.log | cut -c1-400
