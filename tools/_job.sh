@@ -1,3 +1,5 @@
-TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512"
-timeout 2400 $TR bench.py --gpus 4 --config c5 --partition domain --no-cpu-baseline --no-e2e --steps 5 --warmup 3 > gpurun_out/bench_c5_dom4_w.log 2>&1; echo dom4=$?
-grep metric gpurun_out/bench_c5_dom4_w.log | cut -c1-400
+P="python tools/spmm_probe.py --reps 3 --config c2"
+$P --warps 8 > gpurun_out/w_c2_w8.json 2>gpurun_out/w.err
+$P --warps 8 --smem 65536 > gpurun_out/w_c2_w8_s64.json 2>>gpurun_out/w.err
+$P --warps 16 --smem 65536 > gpurun_out/w_c2_w16_s64.json 2>>gpurun_out/w.err
+tail -3 gpurun_out/w.err
