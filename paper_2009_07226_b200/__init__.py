@@ -7,7 +7,9 @@ all on sm_100a kernels in ``libxct_b200.so`` behind a C ABI
 (``include/xct_b200.h``).  There is no CPU fallback.
 """
 
-from . import engine, geometry, hilbert, matrixstore, parallel, pipeline, solver  # noqa: F401
+from . import (cli, dataio, engine, geometry, hilbert, matrixstore, parallel,  # noqa: F401
+               pipeline, solver)
 
 __version__ = "0.1.0"
-__all__ = ["engine", "geometry", "hilbert", "matrixstore", "parallel", "pipeline", "solver"]
+__all__ = ["cli", "dataio", "engine", "geometry", "hilbert", "matrixstore", "parallel",
+           "pipeline", "solver"]
