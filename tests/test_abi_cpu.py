@@ -165,11 +165,16 @@ def test_f64_to_f16_matches_numpy():
     assert np.array_equal(got, vals.astype(np.float16).astype(np.float64))
 
 
+@pytest.mark.parametrize("compress", [False, True])
 @pytest.mark.parametrize("prec", ["single", "mixed"])
 @pytest.mark.parametrize("side", ["forward", "adjoint"])
-def test_bank_conflict_free_schedule(prec, side):
+def test_bank_conflict_free_schedule(prec, side, compress, monkeypatch):
     """Scheduled slabs hold every row's entries exactly once (as a multiset)
-    and no two rows of a quarter-warp read the same bank class in a step."""
+    and no two rows of a quarter-warp read the same bank class in a step
+    (XCT_SCHED_COMPRESS=0); the default compressed schedule keeps the row
+    width and tolerates a few conflicts (< 10% of quarter-steps) instead of
+    extra steps."""
+    monkeypatch.setenv("XCT_SCHED_COMPRESS", "1" if compress else "0")
     g = O.make_geom(40, 1, 32)
     A = O.system_matrix(g)
     ip, ix, v = A.indptr, A.indices.astype(np.int32), A.values
@@ -209,7 +214,10 @@ def test_bank_conflict_free_schedule(prec, side):
                     pairs = set(zip(s_q.tolist(), c_q.tolist()))
                     steps += 1
                     conflicts += len(pairs) - len({c for _, c in pairs})
-    assert conflicts == 0, (conflicts, steps)
+    if compress:
+        assert conflicts <= 0.1 * steps, (conflicts, steps)
+    else:
+        assert conflicts == 0, (conflicts, steps)
 
 
 def replay_grouped(info, a, rows, n_rows):
@@ -241,10 +249,12 @@ def replay_grouped(info, a, rows, n_rows):
 @pytest.mark.parametrize("prec", ["single", "mixed"])
 @pytest.mark.parametrize("side", ["forward", "adjoint"])
 @pytest.mark.parametrize("G", [2, 4])
-def test_grouped_rows_format(prec, side, G):
+def test_grouped_rows_format(prec, side, G, monkeypatch):
     """row_group G: every row's entries appear exactly once with its own
     values (zeros elsewhere), the union is smaller than the sum of the rows,
-    and no two units of a quarter-warp read the same bank class in a step."""
+    and no two units of a quarter-warp read the same bank class in a step
+    (strict schedule)."""
+    monkeypatch.setenv("XCT_SCHED_COMPRESS", "0")
     g = O.make_geom(40, 1, 32)
     A = O.system_matrix(g)
     ip, ix, v = A.indptr, A.indices.astype(np.int32), A.values
