@@ -13,6 +13,8 @@
 // rounded in f32 -- exactly payload.astype(f32) * np.float32(factor).
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "xct_common.h"
 
 namespace {
@@ -29,6 +31,16 @@ __device__ __forceinline__ double load_as_f64(const void* v, int dtype, float f,
 __device__ __forceinline__ float load_f32(const void* v, int dtype, float f, int64_t i) {
   if (dtype == 1) return ((const float*)v)[i];
   return __fmul_rn(__half2float(((const __half*)v)[i]), f);
+}
+
+// 4 consecutive elements at i (multiple of 4) as f32: 16-byte load of f32,
+// 8-byte load of f16 (x factor, rounded in f32 -- as load_f32)
+__device__ __forceinline__ float4 load4_f32(const void* v, int dtype, float f, int64_t i) {
+  if (dtype == 1) return *reinterpret_cast<const float4*>((const float*)v + i);
+  const uint2 h = *reinterpret_cast<const uint2*>((const __half*)v + i);
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&h.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&h.y));
+  return make_float4(__fmul_rn(a.x, f), __fmul_rn(a.y, f), __fmul_rn(b.x, f), __fmul_rn(b.y, f));
 }
 
 __device__ __forceinline__ unsigned long long abs_bits(double x) {
@@ -135,6 +147,25 @@ __global__ void normalize_strided(const void* v, int in_f64, int64_t n, int64_t 
 
 // ---- chunked persistent vectors [n_chunks][n][f_dev] -----------------------
 
+__global__ void chunk_maxabs_chunked_vec_k(const void* v, int dtype, float fv, int64_t per_chunk,
+                                           unsigned long long* maxbits) {
+  const int c = blockIdx.y;
+  const int64_t base = (int64_t)c * per_chunk;
+  unsigned long long m = 0;
+  for (int64_t t = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); t < per_chunk;
+       t += 4 * (int64_t)gridDim.x * blockDim.x) {
+    const float4 x = load4_f32(v, dtype, fv, base + t);
+    const float e[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const unsigned long long b = abs_bits((double)e[k]);
+      m = b > m ? b : m;
+    }
+  }
+  m = block_max(m);
+  if (threadIdx.x == 0 && m) atomicMax(&maxbits[c], m);
+}
+
 __global__ void chunk_maxabs_chunked_k(const void* v, int dtype, float fv, int64_t per_chunk,
                                        unsigned long long* maxbits) {
   const int c = blockIdx.y;
@@ -147,6 +178,30 @@ __global__ void chunk_maxabs_chunked_k(const void* v, int dtype, float fv, int64
   }
   m = block_max(m);
   if (threadIdx.x == 0 && m) atomicMax(&maxbits[c], m);
+}
+
+// f32/f16 input, f32/f16 output, per_chunk % 4 == 0: four elements per step
+template <typename Out>
+__global__ void normalize_chunked_vec_k(const void* v, int dtype, float fv, int64_t per_chunk,
+                                        const double* factors, Out* out) {
+  const int c = blockIdx.y;
+  const int64_t base = (int64_t)c * per_chunk;
+  const float fac = (float)factors[c];
+  for (int64_t t = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); t < per_chunk;
+       t += 4 * (int64_t)gridDim.x * blockDim.x) {
+    const float4 x = load4_f32(v, dtype, fv, base + t);
+    const float e[4] = {__fdiv_rn(x.x, fac), __fdiv_rn(x.y, fac), __fdiv_rn(x.z, fac),
+                        __fdiv_rn(x.w, fac)};
+    if constexpr (sizeof(Out) == 4) {
+      *reinterpret_cast<float4*>((float*)out + base + t) = make_float4(e[0], e[1], e[2], e[3]);
+    } else {
+      __half2 lo = __floats2half2_rn(e[0], e[1]), hi = __floats2half2_rn(e[2], e[3]);
+      uint2 pk;
+      pk.x = *reinterpret_cast<unsigned*>(&lo);
+      pk.y = *reinterpret_cast<unsigned*>(&hi);
+      *reinterpret_cast<uint2*>((__half*)out + base + t) = pk;
+    }
+  }
 }
 
 template <typename Out>
@@ -222,6 +277,60 @@ __global__ void axpy_kernel(const void* a, int at, float fa, const void* b, int 
     m = block_max(m);
     if (threadIdx.x == 0 && m) atomicMax(maxbits, m);
   } else if (mode == 2 && partials) {
+    sq = block_sum(sq);
+    if (threadIdx.x == 0) partials[blockIdx.x] = sq;
+  }
+}
+
+// Vector form of axpy_kernel for f32/f16 operands (n % 4 == 0): the same
+// per-element arithmetic, four consecutive elements per thread and step.
+template <int MODE>
+__global__ void axpy_vec_kernel(const void* a, int at, float fa, const void* b, int bt, float fb,
+                                float s32, int64_t n, void* out, float ofac,
+                                unsigned long long* maxbits, double* partials) {
+  unsigned long long m = 0;
+  double sq = 0.0;
+  for (int64_t i = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); i < n;
+       i += 4 * (int64_t)gridDim.x * blockDim.x) {
+    float4 v = load4_f32(a, at, fa, i);
+    if (b) {
+      const float4 w = load4_f32(b, bt, fb, i);
+      v.x = __fadd_rn(v.x, __fmul_rn(s32, w.x));
+      v.y = __fadd_rn(v.y, __fmul_rn(s32, w.y));
+      v.z = __fadd_rn(v.z, __fmul_rn(s32, w.z));
+      v.w = __fadd_rn(v.w, __fmul_rn(s32, w.w));
+    }
+    if (MODE == 0) {
+      *reinterpret_cast<float4*>((float*)out + i) = v;
+    } else if (MODE == 1) {
+      const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const unsigned long long bb = abs_bits((double)e[k]);
+        m = bb > m ? bb : m;
+      }
+    } else {
+      const __half h0 = __float2half_rn(__fdiv_rn(v.x, ofac));
+      const __half h1 = __float2half_rn(__fdiv_rn(v.y, ofac));
+      const __half h2 = __float2half_rn(__fdiv_rn(v.z, ofac));
+      const __half h3 = __float2half_rn(__fdiv_rn(v.w, ofac));
+      __half2 lo = __halves2half2(h0, h1), hi = __halves2half2(h2, h3);
+      uint2 pk;
+      pk.x = *reinterpret_cast<unsigned*>(&lo);
+      pk.y = *reinterpret_cast<unsigned*>(&hi);
+      *reinterpret_cast<uint2*>((__half*)out + i) = pk;
+      const __half hh[4] = {h0, h1, h2, h3};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double back = (double)__fmul_rn(__half2float(hh[k]), ofac);
+        sq += back * back;
+      }
+    }
+  }
+  if (MODE == 1) {
+    m = block_max(m);
+    if (threadIdx.x == 0 && m) atomicMax(maxbits, m);
+  } else if (MODE == 2 && partials) {
     sq = block_sum(sq);
     if (threadIdx.x == 0) partials[blockIdx.x] = sq;
   }
@@ -332,9 +441,25 @@ extern "C" int xct_axpy(const void* d_a, int a_dtype, float fa, const void* d_b,
   cudaStream_t s = (cudaStream_t)stream;
   int g = blocks_for(n_elem);
   double* partials = (mode == 2 && d_sumsq) ? d_scratch : nullptr;
-  axpy_kernel<<<g, kThreads, 0, s>>>(d_a, a_dtype, fa, d_b, b_dtype, fb, scale, n_elem, d_out,
-                                     out_dtype, out_factor, mode,
-                                     (unsigned long long*)d_maxbits, partials);
+  const bool vec = a_dtype != 0 && n_elem % 4 == 0 && (mode != 0 || out_dtype == 1);
+  if (vec) {
+    const int gv = blocks_for(n_elem / 4);
+    auto* mb = (unsigned long long*)d_maxbits;
+    if (mode == 0)
+      axpy_vec_kernel<0><<<gv, kThreads, 0, s>>>(d_a, a_dtype, fa, d_b, b_dtype, fb, (float)scale,
+                                                 n_elem, d_out, out_factor, mb, partials);
+    else if (mode == 1)
+      axpy_vec_kernel<1><<<gv, kThreads, 0, s>>>(d_a, a_dtype, fa, d_b, b_dtype, fb, (float)scale,
+                                                 n_elem, d_out, out_factor, mb, partials);
+    else
+      axpy_vec_kernel<2><<<gv, kThreads, 0, s>>>(d_a, a_dtype, fa, d_b, b_dtype, fb, (float)scale,
+                                                 n_elem, d_out, out_factor, mb, partials);
+    g = gv;
+  } else {
+    axpy_kernel<<<g, kThreads, 0, s>>>(d_a, a_dtype, fa, d_b, b_dtype, fb, scale, n_elem, d_out,
+                                       out_dtype, out_factor, mode,
+                                       (unsigned long long*)d_maxbits, partials);
+  }
   if (partials) final_sum_kernel<<<1, 1024, 0, s>>>(partials, g, d_sumsq);
   XCT_CUDA_CHECK_LAUNCH("axpy");
   return XCT_OK;
@@ -348,8 +473,14 @@ extern "C" int xct_chunk_maxabs_chunked(const void* d_v, int dtype, float fv, in
   int64_t per = n * f_dev;
   int gx = blocks_for(per);
   if (gx > 512) gx = 512;
-  chunk_maxabs_chunked_k<<<dim3(gx, (unsigned)n_chunks), kThreads, 0, (cudaStream_t)stream>>>(
-      d_v, dtype, fv, per, (unsigned long long*)d_maxbits);
+  if (dtype != 0 && per % 4 == 0) {
+    const int gv = std::max(1, std::min(512, blocks_for(per / 4)));
+    chunk_maxabs_chunked_vec_k<<<dim3(gv, (unsigned)n_chunks), kThreads, 0, (cudaStream_t)stream>>>(
+        d_v, dtype, fv, per, (unsigned long long*)d_maxbits);
+  } else {
+    chunk_maxabs_chunked_k<<<dim3(gx, (unsigned)n_chunks), kThreads, 0, (cudaStream_t)stream>>>(
+        d_v, dtype, fv, per, (unsigned long long*)d_maxbits);
+  }
   XCT_CUDA_CHECK_LAUNCH("chunk_maxabs_chunked");
   return XCT_OK;
 }
@@ -366,7 +497,13 @@ extern "C" int xct_normalize_chunked(const void* d_v, int dtype, float fv, int64
   cudaStream_t s = (cudaStream_t)stream;
   if (precision == XCT_DOUBLE)
     normalize_chunked_k<double><<<grid, kThreads, 0, s>>>(d_v, dtype, fv, per, d_factors, (double*)d_out);
-  else if (precision == XCT_SINGLE)
+  else if (dtype != 0 && per % 4 == 0) {
+    dim3 gv(std::max(1, std::min(512, blocks_for(per / 4))), (unsigned)n_chunks);
+    if (precision == XCT_SINGLE)
+      normalize_chunked_vec_k<float><<<gv, kThreads, 0, s>>>(d_v, dtype, fv, per, d_factors, (float*)d_out);
+    else
+      normalize_chunked_vec_k<__half><<<gv, kThreads, 0, s>>>(d_v, dtype, fv, per, d_factors, (__half*)d_out);
+  } else if (precision == XCT_SINGLE)
     normalize_chunked_k<float><<<grid, kThreads, 0, s>>>(d_v, dtype, fv, per, d_factors, (float*)d_out);
   else
     normalize_chunked_k<__half><<<grid, kThreads, 0, s>>>(d_v, dtype, fv, per, d_factors, (__half*)d_out);

@@ -1,6 +1,6 @@
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-timeout 900 python bench.py > gpurun_out/bench_c2_v15.log 2>&1; echo bench=$?
-timeout 900 python bench.py --config c2m --no-cpu-baseline > gpurun_out/bench_c2m_v15.log 2>&1; echo benchm=$?
-grep metric gpurun_out/bench_c2_v15.log | cut -c1-250
-grep metric gpurun_out/bench_c2m_v15.log | cut -c1-250
+timeout 900 python bench.py > gpurun_out/bench_c2_v16.log 2>&1; echo bench=$?
+timeout 900 python bench.py --config c2m --no-cpu-baseline > gpurun_out/bench_c2m_v16.log 2>&1; echo benchm=$?
+grep metric gpurun_out/bench_c2_v16.log | cut -c1-250
+grep metric gpurun_out/bench_c2m_v16.log | cut -c1-250
