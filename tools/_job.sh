@@ -1,6 +1,5 @@
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-timeout 900 python bench.py > gpurun_out/bench_c2_v16.log 2>&1; echo bench=$?
-timeout 900 python bench.py --config c2m --no-cpu-baseline > gpurun_out/bench_c2m_v16.log 2>&1; echo benchm=$?
-grep metric gpurun_out/bench_c2_v16.log | cut -c1-250
-grep metric gpurun_out/bench_c2m_v16.log | cut -c1-250
+TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29513"
+timeout 1500 $TR bench.py --gpus 4 --config c3 --no-cpu-baseline > gpurun_out/bench_c3_n4.log 2>&1; echo c3=$?
+grep metric gpurun_out/bench_c3_n4.log | cut -c1-300
+timeout 2400 $TR bench.py --gpus 4 --config c5 --partition domain --no-cpu-baseline --no-e2e > gpurun_out/bench_c5_dom4_v16.log 2>&1; echo c5=$?
+grep metric gpurun_out/bench_c5_dom4_v16.log | cut -c1-300
