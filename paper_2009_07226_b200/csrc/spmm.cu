@@ -205,9 +205,8 @@ template <int NPL> struct Acc<XCT_HALF, NPL> {     // fp16 storage and accumulat
   }
 };
 
-// CONTRACT (native order only): one FFMA per slice instead of the
-// reference's multiply-then-add -- a single rounding, half the FP issue.
-template <int NPL, bool CONTRACT> struct Acc<XCT_SINGLE, NPL, CONTRACT> {
+// FP32, reference rounding: multiply then add (two roundings) per slice.
+template <int NPL> struct Acc<XCT_SINGLE, NPL, false> {
   static constexpr int V = 4;
   float a[4 * NPL];
   __device__ void zero() {
@@ -217,14 +216,35 @@ template <int NPL, bool CONTRACT> struct Acc<XCT_SINGLE, NPL, CONTRACT> {
   __device__ void fma(int q, const uint4& r, float len) {
     const unsigned w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if constexpr (CONTRACT)
-        a[4 * q + i] = __fmaf_rn(__uint_as_float(w[i]), len, a[4 * q + i]);
-      else
-        a[4 * q + i] = __fadd_rn(a[4 * q + i], __fmul_rn(__uint_as_float(w[i]), len));
-    }
+    for (int i = 0; i < 4; ++i)
+      a[4 * q + i] = __fadd_rn(a[4 * q + i], __fmul_rn(__uint_as_float(w[i]), len));
   }
   __device__ float out(int i, float scale) const { return a[i] * scale; }
+};
+
+// CONTRACT (native order only): one rounding per slice, issued as packed
+// FFMA2 (fma.rn.f32x2, sm_100a) on slice pairs with the entry's length
+// broadcast -- half the FP issue slots of scalar FFMA.
+template <int NPL> struct Acc<XCT_SINGLE, NPL, true> {
+  static constexpr int V = 4;
+  unsigned long long a[2 * NPL];                   // slice pairs
+  __device__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 2 * NPL; ++i) a[i] = 0ull;
+  }
+  __device__ void fma(int q, const uint4& r, float len) {
+    unsigned long long x0, x1, l2;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x0) : "r"(r.x), "r"(r.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x1) : "r"(r.z), "r"(r.w));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(l2) : "f"(len));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a[2 * q]) : "l"(x0), "l"(l2));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a[2 * q + 1]) : "l"(x1), "l"(l2));
+  }
+  __device__ float out(int i, float scale) const {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a[i >> 1]));
+    return ((i & 1) ? hi : lo) * scale;
+  }
 };
 
 template <int NPL> struct Acc<XCT_DOUBLE, NPL> {   // fp64 storage and accumulate

@@ -1,5 +1,4 @@
-TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29513"
-timeout 1500 $TR bench.py --gpus 4 --config c3 --no-cpu-baseline > gpurun_out/bench_c3_n4.log 2>&1; echo c3=$?
-grep metric gpurun_out/bench_c3_n4.log | cut -c1-300
-timeout 2400 $TR bench.py --gpus 4 --config c5 --partition domain --no-cpu-baseline --no-e2e > gpurun_out/bench_c5_dom4_v16.log 2>&1; echo c5=$?
-grep metric gpurun_out/bench_c5_dom4_v16.log | cut -c1-300
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+python tools/spmm_probe.py --reps 3 --config c2 > gpurun_out/y_c2_ffma2.json 2>gpurun_out/y.err
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_c2_v17.log 2>&1; echo bench=$?
+grep metric gpurun_out/bench_c2_v17.log | cut -c1-250
