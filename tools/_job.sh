@@ -1,4 +1,3 @@
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-python tools/spmm_probe.py --reps 3 --config c2 > gpurun_out/y_c2_ffma2.json 2>gpurun_out/y.err
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_c2_v17.log 2>&1; echo bench=$?
-grep metric gpurun_out/bench_c2_v17.log | cut -c1-250
+XCT_FWD_WARP_VIEWS=1 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k grouped > gpurun_out/pytest_grouped.log 2>&1; echo pytest=$?
+XCT_FWD_WARP_VIEWS=1 python tools/spmm_probe.py --reps 3 --config c2 > gpurun_out/v2_c2_wv.json 2>gpurun_out/v2.err
+tail -3 gpurun_out/v2.err

@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--ppl", type=int, default=None)
     ap.add_argument("--groups", default="16", help="chunk_group values to sweep")
     ap.add_argument("--row-group", type=int, default=None)
+    ap.add_argument("--ffactor", type=int, default=16)
     ap.add_argument("--contract", default="auto", help="auto | 0 | 1 | sweep")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -46,7 +47,7 @@ def main():
     g = geometry.make_geometry(cfg["k"], S, cfg["n"])
     t0 = time.perf_counter()
     system = pipeline.assemble(g, pipeline.SystemConfig(
-        precision=cfg["precision"], ffactor=16, order=args.order, warps_per_cta=args.warps,
+        precision=cfg["precision"], ffactor=args.ffactor, order=args.order, warps_per_cta=args.warps,
         smem_budget=args.smem, pieces_per_lane=args.ppl, row_group=args.row_group))
     t_asm = time.perf_counter() - t0
     nnz = system.matrix.nnz
@@ -61,7 +62,7 @@ def main():
            "assemble_s": t_asm, "warps": args.warps, "smem": args.smem, "ppl": args.ppl}
     for name, side in (("forward", system.forward), ("adjoint", system.adjoint)):
         blk = side.blocks[0]
-        n_chunks = -(-S // 16)
+        n_chunks = -(-S // args.ffactor)
         x = (torch.rand((n_chunks, blk.n_in, blk.f_dev), device=dev) * 0.5).to(sd)
         y = torch.empty((n_chunks, blk.n_out, blk.f_dev), dtype=od, device=dev)
         fac = torch.ones(n_chunks, dtype=torch.float64, device=dev)
