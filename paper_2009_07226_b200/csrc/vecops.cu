@@ -595,6 +595,60 @@ __global__ void scale_chunks_k(T* v, int64_t per_chunk, int64_t n_chunks, const 
     if (threadIdx.x == 0) partials[blockIdx.x] = sq;
   }
 }
+// f32 rows of fd % 4 == 0 floats: one float4 per thread step, chunk =
+// blockIdx.y, 32-bit row / piece arithmetic (fd/4 is a power of two)
+__global__ void gather_rows_v4(const float4* src, int64_t n_src, const int32_t* idx, int m,
+                               int lq, float4* dst) {
+  const int c = blockIdx.y;
+  const int total = m << lq;
+  const float4* s = src + (int64_t)c * n_src * (1 << lq);
+  float4* d = dst + (int64_t)c * total;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int i = t >> lq, q = t & ((1 << lq) - 1);
+    d[t] = s[((int64_t)idx[i] << lq) + q];
+  }
+}
+
+__global__ void accumulate_rows_v4(float4* dst, int64_t n_dst, const float4* src,
+                                   const int32_t* pos, int m, int lq) {
+  const int c = blockIdx.y;
+  const int total = m << lq;
+  const float4* s = src + (int64_t)c * total;
+  float4* d = dst + (int64_t)c * n_dst * (1 << lq);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int i = t >> lq, q = t & ((1 << lq) - 1);
+    float4* o = d + ((int64_t)pos[i] << lq) + q;
+    float4 a = *o;
+    const float4 b = s[t];
+    a.x = a.x + b.x; a.y = a.y + b.y; a.z = a.z + b.z; a.w = a.w + b.w;
+    *o = a;
+  }
+}
+
+__global__ void scale_chunks_v4(float4* v, int64_t per4, const double* factors, double* partials) {
+  const int c = blockIdx.y;
+  const float f = (float)factors[c];
+  float4* p = v + (int64_t)c * per4;
+  double sq = 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < per4;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    float4 x = p[t];
+    x.x = x.x * f; x.y = x.y * f; x.z = x.z * f; x.w = x.w * f;
+    p[t] = x;
+    sq += (double)x.x * x.x + (double)x.y * x.y + (double)x.z * x.z + (double)x.w * x.w;
+  }
+  if (partials) {
+    sq = block_sum(sq);
+    if (threadIdx.x == 0) partials[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = sq;
+  }
+}
+
+int log2_exact(int v) {
+  int l = 0;
+  while ((1 << l) < v) ++l;
+  return (1 << l) == v ? l : -1;
+}
+
 }  // namespace
 
 extern "C" int xct_gather_rows(const void* d_src, int64_t n_src, const int32_t* d_idx, int64_t m,
@@ -604,7 +658,12 @@ extern "C" int xct_gather_rows(const void* d_src, int64_t n_src, const int32_t* 
   const int64_t total = n_chunks * m * fd;
   if (total == 0) return XCT_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (f64) gather_rows_k<double><<<blocks_for(total), kThreads, 0, s>>>((const double*)d_src, n_src, d_idx, m, n_chunks, fd, (double*)d_dst);
+  const int lq = fd % 4 == 0 ? log2_exact(fd / 4) : -1;
+  if (!f64 && lq >= 0 && (m << lq) < (1LL << 31) && n_chunks <= 65535) {
+    dim3 g(std::max(1, std::min(512, blocks_for(m << lq))), (unsigned)n_chunks);
+    gather_rows_v4<<<g, kThreads, 0, s>>>((const float4*)d_src, n_src, d_idx, (int)m, lq,
+                                          (float4*)d_dst);
+  } else if (f64) gather_rows_k<double><<<blocks_for(total), kThreads, 0, s>>>((const double*)d_src, n_src, d_idx, m, n_chunks, fd, (double*)d_dst);
   else gather_rows_k<float><<<blocks_for(total), kThreads, 0, s>>>((const float*)d_src, n_src, d_idx, m, n_chunks, fd, (float*)d_dst);
   XCT_CUDA_CHECK_LAUNCH("gather_rows");
   return XCT_OK;
@@ -618,7 +677,12 @@ extern "C" int xct_accumulate_rows(void* d_dst, int64_t n_dst, const void* d_src
   const int64_t total = n_chunks * m * fd;
   if (total == 0) return XCT_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (f64) accumulate_rows_k<double><<<blocks_for(total), kThreads, 0, s>>>((double*)d_dst, n_dst, (const double*)d_src, d_pos, m, n_chunks, fd);
+  const int lq = fd % 4 == 0 ? log2_exact(fd / 4) : -1;
+  if (!f64 && lq >= 0 && (m << lq) < (1LL << 31) && n_chunks <= 65535) {
+    dim3 g(std::max(1, std::min(512, blocks_for(m << lq))), (unsigned)n_chunks);
+    accumulate_rows_v4<<<g, kThreads, 0, s>>>((float4*)d_dst, n_dst, (const float4*)d_src, d_pos,
+                                              (int)m, lq);
+  } else if (f64) accumulate_rows_k<double><<<blocks_for(total), kThreads, 0, s>>>((double*)d_dst, n_dst, (const double*)d_src, d_pos, m, n_chunks, fd);
   else accumulate_rows_k<float><<<blocks_for(total), kThreads, 0, s>>>((float*)d_dst, n_dst, (const float*)d_src, d_pos, m, n_chunks, fd);
   XCT_CUDA_CHECK_LAUNCH("accumulate_rows");
   return XCT_OK;
@@ -635,8 +699,19 @@ extern "C" int xct_scale_chunks(void* d_v, int64_t per_chunk, int64_t n_chunks,
     if (d_sumsq) cudaMemsetAsync(d_sumsq, 0, sizeof(double), s);
     return XCT_OK;
   }
-  const int g = blocks_for(total);
   double* partials = d_sumsq ? d_scratch : nullptr;
+  if (!f64 && per_chunk % 4 == 0 && n_chunks <= 65535) {
+    // partials: gx per chunk, gx * n_chunks <= kRedBlocks (the scratch size)
+    const int gx = std::max(1, std::min(blocks_for(per_chunk / 4), (int)(kRedBlocks / n_chunks)));
+    if (gx * n_chunks <= kRedBlocks) {
+      scale_chunks_v4<<<dim3(gx, (unsigned)n_chunks), kThreads, 0, s>>>(
+          (float4*)d_v, per_chunk / 4, d_factors, partials);
+      if (partials) final_sum_kernel<<<1, 1024, 0, s>>>(partials, gx * (int)n_chunks, d_sumsq);
+      XCT_CUDA_CHECK_LAUNCH("scale_chunks");
+      return XCT_OK;
+    }
+  }
+  const int g = blocks_for(total);
   if (f64) scale_chunks_k<double><<<g, kThreads, 0, s>>>((double*)d_v, per_chunk, n_chunks, d_factors, partials);
   else scale_chunks_k<float><<<g, kThreads, 0, s>>>((float*)d_v, per_chunk, n_chunks, d_factors, partials);
   if (partials) final_sum_kernel<<<1, 1024, 0, s>>>(partials, g, d_sumsq);

@@ -115,6 +115,37 @@ class NcclComm:
         return float(self._s.item())
 
 
+class _ExchangeProfile:
+    """XCT_EXCHANGE_PROFILE=1: per-phase device times of one partitioned
+    application (phases serialized; a diagnosis aid, not a timing mode)."""
+
+    def __init__(self, rank):
+        import os
+        self.on = os.environ.get("XCT_EXCHANGE_PROFILE") == "1"
+        self.rank, self.laps = rank, []
+        if self.on:
+            import time
+            import torch
+            torch.cuda.synchronize()
+            self.t = time.perf_counter()
+
+    def lap(self, what):
+        if not self.on:
+            return
+        import time
+        import torch
+        torch.cuda.synchronize()
+        now = time.perf_counter()
+        self.laps.append((what, now - self.t))
+        self.t = now
+
+    def report(self, side):
+        if self.on and self.rank == 0:
+            import sys
+            print(f"[xct] exchange {side}: " +
+                  ", ".join(f"{w} {t * 1e3:.1f} ms" for w, t in self.laps), file=sys.stderr)
+
+
 class _DistSide:
     """One direction of the partitioned operator on this rank: the local
     staged block (rows = footprint elements) and the exchange that turns its
@@ -177,6 +208,9 @@ class _DistSide:
                       idx.numel(), c1 - c0, fd, f64, buf.data_ptr(), cg.st)
             return buf
 
+        prof = _ExchangeProfile(self.rank)
+        if prof.on:
+            bounds = [(0, C)]         # phases serialized and timed (diagnosis only)
         pending = []
         for c0, c1 in bounds:
             if ev is not None:
@@ -189,13 +223,19 @@ class _DistSide:
             if ev is not None:
                 e1.record()
                 ev.append((self is cg.sys.forward, e0, e1, (c1 - c0) / C))
+            prof.lap("K6")
             sends = {q: gather(idx, c0, c1) for q, idx in self.send.items()}
+            prof.lap("gather")
             recvs = {s: torch.empty((c1 - c0, idx.numel(), fd), dtype=cg.out_dt,
                                     device=cg.dev)
                      for s, idx in self.recv.items()}
             ops = [dist.P2POp(dist.isend, b, q) for q, b in sends.items()]
             ops += [dist.P2POp(dist.irecv, b, s) for s, b in recvs.items()]
             works = dist.batch_isend_irecv(ops) if ops else []
+            if prof.on:
+                for r in works:
+                    r.wait()
+            prof.lap(f"nccl p2p {sum(b.numel() * b.element_size() for b in sends.values()) / 1e9:.2f} GB out")
             pending.append((c0, c1, works, sends, recvs))
         for c0, c1, works, sends, recvs in pending:
             ow = o[c0:c1]
@@ -209,8 +249,11 @@ class _DistSide:
                 _lib.call("xct_accumulate_rows", ow.data_ptr(), self.num_outputs,
                           recvs[s].data_ptr(), self.recv[s].data_ptr(), self.recv[s].numel(),
                           c1 - c0, fd, f64, cg.st)
+        prof.lap("accumulate")
         _lib.call("xct_scale_chunks", o.data_ptr(), self.num_outputs * fd, C, fac.data_ptr(), f64,
                   cg.scratch.data_ptr(), cg.scal.data_ptr(), cg.st)
+        prof.lap("scale")
+        prof.report("forward" if self is cg.sys.forward else "adjoint")
         return float(cg.scal[0].item())
 
 
