@@ -181,7 +181,8 @@ class _DistSide:
 
     # F-chunk waves per application: the exchange of wave w (gather, NCCL
     # p2p over NVLink) runs on NCCL's stream while K6 computes wave w + 1
-    WAVES = 4
+    import os as _os
+    WAVES = int(_os.environ.get("XCT_EXCHANGE_WAVES", "4"))
 
     def exchange_apply(self, cg, xin, out, fac) -> float:
         """Local partial SpMM, exchange, reduction in the reference's direct
