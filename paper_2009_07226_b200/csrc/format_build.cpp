@@ -289,8 +289,11 @@ namespace {
 // ordered by (key, column) -- ascending ray id per voxel for the back
 // projection -- then placed on slab steps by the bank schedule.
 // Slab layout per (group, warp): slots [width/4][units_per_warp][4] (as for
-// G = 1) and values [width/4][units_per_warp][4][G]: a unit's step is one
-// contiguous run of 4*G values (NV 16-byte pieces at immediate offsets).
+// G = 1) and values [width/4][NV][units_per_warp][16 B], NV = 4*G*vbytes/16:
+// piece k of a unit holds its value words k*epp.., word = entry*G + row.
+// A warp's step is then two contiguous runs (slots, values) that one bulk
+// copy each moves into shared memory, and every 128-bit read of piece k by
+// the warp's units is one conflict-free contiguous run.
 struct UEnt {
   int32_t key, col, dup, slot;
   int64_t j[4];
@@ -554,12 +557,16 @@ int build_grouped(int64_t n_rows, int64_t n_cols, const int64_t* indptr, const i
       const int64_t at = F->slab_off[gg * warps + w] + ((n >> 2) * upw + uin) * 4 + (n & 3);
       F->slots[at] = (uint16_t)slot;
       if (!E) return;                          // padding: values stay 0
+      const int64_t epp = 16 / vbytes;                        // values per piece
+      const int64_t step0 = F->slab_off[gg * warps + w] + (n >> 2) * upw * 4;
       for (int gi = 0; gi < G; ++gi) {
         const int64_t j = E->j[gi];
         if (j < 0) continue;
         const double v = values[j] * scale;
         double back;
-        uint8_t* dst = F->values.get() + (at * G + gi) * vbytes;
+        const int64_t wd = (n & 3) * G + gi;                     // word of the unit's step
+        const int64_t vi = step0 * G + ((wd / epp) * upw + uin) * epp + wd % epp;
+        uint8_t* dst = F->values.get() + vi * vbytes;
         if (precision == XCT_SINGLE) {
           float f = (float)v;
           std::memcpy(dst, &f, 4);

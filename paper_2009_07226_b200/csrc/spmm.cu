@@ -26,6 +26,8 @@
 // HMUL2 then HADD2.
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "xct_common.h"
 
 namespace {
@@ -524,10 +526,18 @@ template <int G> struct GStep<XCT_SINGLE, G> {
   uint2 s;
   uint4 v[NV];
   // sp: this unit's 4 slots of the step; vp: its NV value pieces
-  __device__ void load(const uint16_t* sp, const uint4* vp, uint64_t pol) {
+  // sp: this unit's 4 slots of the step; vp: its first value piece, piece k
+  // upw pieces further (values [NV][units][16 B] per step)
+  __device__ void load(const uint16_t* sp, const uint4* vp, int upw, uint64_t pol) {
     s = ld_stream_u2(sp, pol);
 #pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = ld_stream_u4(vp + k, pol);
+    for (int k = 0; k < NV; ++k) v[k] = ld_stream_u4(vp + (int64_t)k * upw, pol);
+  }
+  // the same step from a shared-memory copy of the warp's step at `base`
+  __device__ void lds(uint32_t base, uint32_t slot_bytes, int uin, int upw) {
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(s.x), "=r"(s.y) : "r"(base + uin * 8));
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = lds128(base + slot_bytes + (uint32_t)(k * upw + uin) * 16u);
   }
   __device__ uint32_t off(int e) const {
     uint32_t q = e < 2 ? s.x : s.y;
@@ -545,10 +555,18 @@ template <int G> struct GStep<XCT_MIXED, G> {
   uint2 s;
   uint4 v[NV];
   // sp: this unit's 4 slots of the step; vp: its NV value pieces
-  __device__ void load(const uint16_t* sp, const uint4* vp, uint64_t pol) {
+  // sp: this unit's 4 slots of the step; vp: its first value piece, piece k
+  // upw pieces further (values [NV][units][16 B] per step)
+  __device__ void load(const uint16_t* sp, const uint4* vp, int upw, uint64_t pol) {
     s = ld_stream_u2(sp, pol);
 #pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = ld_stream_u4(vp + k, pol);
+    for (int k = 0; k < NV; ++k) v[k] = ld_stream_u4(vp + (int64_t)k * upw, pol);
+  }
+  // the same step from a shared-memory copy of the warp's step at `base`
+  __device__ void lds(uint32_t base, uint32_t slot_bytes, int uin, int upw) {
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(s.x), "=r"(s.y) : "r"(base + uin * 8));
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = lds128(base + slot_bytes + (uint32_t)(k * upw + uin) * 16u);
   }
   __device__ uint32_t off(int e) const {
     uint32_t q = e < 2 ? s.x : s.y;
@@ -583,7 +601,31 @@ template <int PREC, int NPL, int G> struct RingDepth {
   static constexpr int value = acc + 4 * nv * 3 <= 72 ? 4 : acc + 4 * nv * 2 <= 80 ? 3 : 2;
 };
 
-template <int PREC, int NPL, int G, bool CONTRACT>
+// mbarrier + bulk-copy helpers (the BULK entry ring)
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar, uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+               " [%0], [%1], %2, [%3], %4;"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  } while (!done);
+}
+
+constexpr int kBulkRing = 6;     // steps of a warp's entry stream in flight
+
+template <int PREC, int NPL, int G, bool CONTRACT, bool BULK>
 __global__ void __launch_bounds__(512) spmm_grouped_kernel(const Params p) {
   using A = Acc<PREC, NPL, CONTRACT>;
   using St = GStep<PREC, G>;
@@ -621,14 +663,45 @@ __global__ void __launch_bounds__(512) spmm_grouped_kernel(const Params p) {
   // Load pointers run D steps ahead: slots + position, values + position/4
   // * NV pieces (a unit's step = NV contiguous pieces).
   const uint16_t* lsp = p.slots + at;
-  const uint4* lvp = reinterpret_cast<const uint4*>(p.values) + at / 4 * St::NV;
+  const uint4* lvp = reinterpret_cast<const uint4*>(p.values) + (at - 4 * uin) / 4 * St::NV + uin;
   const int64_t vstep = (int64_t)St::NV * upw;
-  St r[D];
+  St r[BULK ? 1 : D];
+  if constexpr (!BULK) {
 #pragma unroll
-  for (int i = 0; i < D; ++i) {
-    r[i].load(lsp, lvp, pol_e);
-    lsp += step;
-    lvp += vstep;
+    for (int i = 0; i < D; ++i) {
+      r[i].load(lsp, lvp, upw, pol_e);
+      lsp += step;
+      lvp += vstep;
+    }
+  }
+  // BULK: the warp's entry stream (slots, values) goes through a
+  // kBulkRing-step shared-memory ring filled by cp.async.bulk with one
+  // mbarrier per ring slot -- no registers hold loads in flight.
+  const uint32_t slot_bytes = (uint32_t)upw * 8u;
+  const uint32_t step_bytes = slot_bytes + (uint32_t)upw * St::NV * 16u;
+  const uint32_t ring_off = (2 * bb + 2u * (uint32_t)p.plane_slots * 4u + 127u) & ~127u;
+  const uint32_t ring = s0 + ring_off + (uint32_t)warp * kBulkRing * step_bytes;
+  const uint32_t bars = s0 + ring_off + (uint32_t)(blockDim.x >> 5) * kBulkRing * step_bytes +
+                        (uint32_t)warp * kBulkRing * 8u;
+  const int64_t pos0 = g0 < g1 ? p.slab_off[(int64_t)g0 * p.warps_per_cta + warp] : 0;
+  const char* gsl = reinterpret_cast<const char*>(p.slots + pos0);
+  const char* gvl = reinterpret_cast<const char*>(p.values) + pos0 * G * (PREC == XCT_SINGLE ? 4 : 2);
+  int64_t total = 0;
+  if constexpr (BULK) {
+    for (int gg = g0; gg < g1; ++gg) total += p.slab_width[(int64_t)gg * p.warps_per_cta + warp] >> 2;
+    if (lane == 0) {
+      for (int k = 0; k < kBulkRing; ++k) mbar_init(bars + 8u * k, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int64_t k = 0; k < kBulkRing && k < total; ++k) {
+        mbar_expect_tx(bars + 8u * (uint32_t)k, step_bytes);
+        bulk_g2s(ring + (uint32_t)k * step_bytes, gsl + k * slot_bytes, slot_bytes,
+                 bars + 8u * (uint32_t)k, pol_e);
+        bulk_g2s(ring + (uint32_t)k * step_bytes + slot_bytes,
+                 gvl + k * (int64_t)(step_bytes - slot_bytes), step_bytes - slot_bytes,
+                 bars + 8u * (uint32_t)k, pol_e);
+      }
+    }
+    __syncwarp();
   }
   int32_t* const maps = reinterpret_cast<int32_t*>(
       reinterpret_cast<char*>(stage) + 2 * (size_t)bb);
@@ -667,18 +740,47 @@ __global__ void __launch_bounds__(512) spmm_grouped_kernel(const Params p) {
 #pragma unroll
     for (int qq = 0; qq < NPL; ++qq) pb[qq] = s0 + (odd ? bb : 0u) + pbase[qq];
   };
-  for (;;) {
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      while (left == 0) {
-        if (++g >= g1) goto done;
-        enter(g);
+  if constexpr (BULK) {
+    auto fetch = [&](int64_t k, St& out) {
+      const uint32_t sl = (uint32_t)(k % kBulkRing);
+      mbar_wait(bars + 8u * sl, (uint32_t)((k / kBulkRing) & 1));
+      out.lds(ring + sl * step_bytes, slot_bytes, uin, upw);
+    };
+    St cur, nxt;
+    if (total > 0) fetch(0, cur);
+    for (int64_t k = 0; k < total; ++k) {
+      while (left == 0) enter(++g);
+      if (k + 1 < total) fetch(k + 1, nxt);
+      consume_g<NPL, G>(acc, cur, pb);
+      __syncwarp();                     // every lane is done with ring slot k
+      const int64_t kn = k + kBulkRing;
+      if (lane == 0 && kn < total) {
+        const uint32_t sl = (uint32_t)(k % kBulkRing);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bars + 8u * sl, step_bytes);
+        bulk_g2s(ring + sl * step_bytes, gsl + kn * slot_bytes, slot_bytes, bars + 8u * sl, pol_e);
+        bulk_g2s(ring + sl * step_bytes + slot_bytes,
+                 gvl + kn * (int64_t)(step_bytes - slot_bytes), step_bytes - slot_bytes,
+                 bars + 8u * sl, pol_e);
       }
-      consume_g<NPL, G>(acc, r[i], pb);
-      r[i].load(lsp, lvp, pol_e);
-      lsp += step;
-      lvp += vstep;
+      cur = nxt;
       --left;
+    }
+    while (++g < g1) enter(g);          // trailing groups empty for this warp
+  } else {
+    for (;;) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        while (left == 0) {
+          if (++g >= g1) goto done;
+          enter(g);
+        }
+        consume_g<NPL, G>(acc, r[i], pb);
+        r[i].load(lsp, lvp, upw, pol_e);
+        lsp += step;
+        lvp += vstep;
+        --left;
+      }
     }
   }
 done:
@@ -717,11 +819,11 @@ done:
   }
 }
 
-template <int PREC, int NPL, int G, bool CONTRACT>
+template <int PREC, int NPL, int G, bool CONTRACT, bool BULK>
 int launch_grouped(const Params& p, int64_t n_chunks, int threads, int64_t smem, cudaStream_t s) {
   static int configured = -1;
   if (configured < (int)smem) {
-    cudaError_t e = cudaFuncSetAttribute(spmm_grouped_kernel<PREC, NPL, G, CONTRACT>,
+    cudaError_t e = cudaFuncSetAttribute(spmm_grouped_kernel<PREC, NPL, G, CONTRACT, BULK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
       return xct::fail(XCT_ECUDA, std::string("spmm smem attribute: ") + cudaGetErrorString(e));
@@ -730,18 +832,35 @@ int launch_grouped(const Params& p, int64_t n_chunks, int threads, int64_t smem,
   if (threads > 512) return xct::fail(XCT_EINVAL, "spmm: grouped rows need <= 16 warps per CTA");
   const int64_t n_blocks = (int64_t)p.n_cta * n_chunks;
   if (n_blocks > 0x7fffffffLL) return xct::fail(XCT_EINVAL, "spmm: grid too large");
-  spmm_grouped_kernel<PREC, NPL, G, CONTRACT><<<(unsigned)n_blocks, threads, smem, s>>>(p);
+  spmm_grouped_kernel<PREC, NPL, G, CONTRACT, BULK><<<(unsigned)n_blocks, threads, smem, s>>>(p);
   XCT_CUDA_CHECK_LAUNCH("spmm_grouped");
   return XCT_OK;
+}
+
+template <int PREC, bool CONTRACT, bool BULK>
+int launch_grouped_b(const Params& p, int npl, int G, int64_t n_chunks, int threads,
+                     int64_t smem, cudaStream_t s) {
+  if (npl == 1 && G == 2) return launch_grouped<PREC, 1, 2, CONTRACT, BULK>(p, n_chunks, threads, smem, s);
+  if (npl == 1 && G == 4) return launch_grouped<PREC, 1, 4, CONTRACT, BULK>(p, n_chunks, threads, smem, s);
+  if (npl == 2 && G == 2) return launch_grouped<PREC, 2, 2, CONTRACT, BULK>(p, n_chunks, threads, smem, s);
+  if (npl == 2 && G == 4) return launch_grouped<PREC, 2, 4, CONTRACT, BULK>(p, n_chunks, threads, smem, s);
+  return xct::fail(XCT_EINVAL, "spmm: grouped rows need G in {2, 4} and 1 or 2 pieces per lane");
+}
+
+// The register ring is the default; XCT_SPMM_BULK=1 selects the bulk-copy
+// shared-memory entry ring (measured slower at c2: 80.7 / 64.6 ms vs 61.7 /
+// 48.8 ms -- the extra shared-memory traffic and per-step mbarrier waits
+// cost more than the load latency they hide; profiles/r01_probe_c2_bulk*).
+bool use_bulk() {
+  const char* e = std::getenv("XCT_SPMM_BULK");
+  return e && e[0] == '1';
 }
 
 template <int PREC, bool CONTRACT>
 int launch_grouped_npl(const Params& p, int npl, int G, int64_t n_chunks, int threads,
                        int64_t smem, cudaStream_t s) {
-  if (npl == 1 && G == 2) return launch_grouped<PREC, 1, 2, CONTRACT>(p, n_chunks, threads, smem, s);
-  if (npl == 1 && G == 4) return launch_grouped<PREC, 1, 4, CONTRACT>(p, n_chunks, threads, smem, s);
-  if (npl == 2 && G == 2) return launch_grouped<PREC, 2, 2, CONTRACT>(p, n_chunks, threads, smem, s);
-  if (npl == 2 && G == 4) return launch_grouped<PREC, 2, 4, CONTRACT>(p, n_chunks, threads, smem, s);
+  if (use_bulk()) return launch_grouped_b<PREC, CONTRACT, true>(p, npl, G, n_chunks, threads, smem, s);
+  return launch_grouped_b<PREC, CONTRACT, false>(p, npl, G, n_chunks, threads, smem, s);
   return xct::fail(XCT_EINVAL, "spmm: grouped rows need G in {2, 4} and 1 or 2 pieces per lane");
 }
 
@@ -783,8 +902,15 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   if (threads < 32 || threads > 1024) return xct::fail(XCT_EINVAL, "spmm: CTA must have 1..32 warps");
   const int64_t plane_slots = (a->max_group_slots + 7) & ~(int64_t)7;
   if (plane_slots * 16 > 65536) return xct::fail(XCT_ESTAGE, "spmm: plane offsets exceed 16 bits");
-  // double-buffered stage + two slot->element maps
-  const int64_t need = 2 * ((plane_slots << (lp + 4)) + 128) + 2 * plane_slots * 4;
+  // double-buffered stage + two slot->element maps (+ the grouped kernel's
+  // per-warp bulk entry ring and its mbarriers, 128-byte aligned)
+  int64_t need = 2 * ((plane_slots << (lp + 4)) + 128) + 2 * plane_slots * 4;
+  if (G > 1 && use_bulk()) {
+    const int64_t upw_ = a->rows_per_warp / G;
+    const int64_t nv = 4 * G * (precision == XCT_SINGLE ? 4 : 2) / 16;
+    const int64_t step_b = upw_ * 8 + upw_ * nv * 16;
+    need = ((need + 127) & ~(int64_t)127) + a->warps_per_cta * kBulkRing * (step_b + 8);
+  }
   if (smem_bytes < need) smem_bytes = need;
   if (smem_bytes > 227 * 1024) return xct::fail(XCT_ESTAGE, "spmm: load group exceeds shared memory");
 

@@ -227,6 +227,7 @@ def replay_grouped(info, a, rows, n_rows):
     seqs = {r: [] for r in range(n_rows)}
     rpw, w = info.rows_per_warp, info.warps_per_cta
     upw = rpw // G
+    epp = 16 // info.value_bytes
     for b in range(info.n_cta):
         for g in range(a["gp"][b], a["gp"][b + 1]):
             gmap = a["m"][a["mp"][g]:a["mp"][g + 1]]
@@ -236,9 +237,11 @@ def replay_grouped(info, a, rows, n_rows):
                 for u in range(upw):
                     for n in range(width):
                         at = off + ((n // 4) * upw + u) * 4 + n % 4
+                        step0 = off + (n // 4) * upw * 4
                         for gi in range(G):
                             r = rows[b, (wi * upw + u) * G + gi]
-                            val = a["v"][at * G + gi]
+                            wd = (n % 4) * G + gi         # values [NV][units][16 B]
+                            val = a["v"][step0 * G + ((wd // epp) * upw + u) * epp + wd % epp]
                             if r < 0:
                                 assert val == 0
                             elif val != 0:
