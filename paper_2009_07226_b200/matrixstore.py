@@ -47,6 +47,7 @@ DEFAULT_STAGE_CAPACITY = 96 * 1024      # src/matrixstore.py:44
 SAFE_MAX = 60000.0                      # src/matrixstore.py:46
 SMEM_BUDGET = 96 * 1024                 # per CTA: two resident CTAs per SM
 SMEM_MAX = 224 * 1024                   # opt-in maximum per CTA on sm_100a
+GROUPED_SMEM_BUDGET = 192 * 1024        # grouped rows: one CTA per SM
 
 _STORE = {"double": np.float64, "single": np.float32, "half": np.float16, "mixed": np.float16}
 _COMPUTE = {"double": np.float64, "single": np.float32, "half": np.float16, "mixed": np.float32}
@@ -441,7 +442,8 @@ def build_format(indptr: np.ndarray, indices32: np.ndarray, values: np.ndarray,
     f_dev = f_dev_for(ffactor, precision)
     rec = f_dev * element_bytes(precision)
     # the kernel double-buffers the stage: two groups of `capacity` records
-    capacity = min(65536, max(1, smem_budget // (2 * rec)))
+    # K6 addresses a staged record by a 16-bit byte offset (slot * 16)
+    capacity = min(65536 // 16, max(1, smem_budget // (2 * rec)))
     rows = np.ascontiguousarray(plan.cta_rows, np.int32)
     keys = np.ascontiguousarray(plan.key_tables, np.int32)
     ctab = np.ascontiguousarray(plan.cta_table, np.int32)

@@ -327,7 +327,7 @@ class DomainPartitionedSystem:
                         budget = pipeline.smem_budget_for(config, plan)
                     else:
                         plan = matrixstore.restrict_plan(gplan, rows_g, cols_g)
-                        budget = config.smem_budget
+                        budget = config.smem_budget_effective
                     sides.append(matrixstore.build_format(pip, pix, pv, nr, nc, plan,
                                                           config.precision, config.ffactor,
                                                           exp, budget, schedule))
@@ -489,7 +489,7 @@ def build_rank_blocks_streamed(g, config, tomo, sino, rank, dev, n_threads=None)
             g.angles, n)
         plan = matrixstore.restrict_plan(gplan, fp, cols)
         hf = matrixstore.build_format(bip, bix, bv, len(fp), len(cols), plan, config.precision,
-                                      config.ffactor, exp, config.smem_budget, schedule)
+                                      config.ffactor, exp, config.smem_budget_effective, schedule)
         hf.cta_rows = np.where(hf.cta_rows >= 0, hf.cta_rows + base, -1).astype(np.int32)
         fparts.append(hf)
         fps.append(fp)
@@ -533,7 +533,7 @@ def build_rank_blocks_streamed(g, config, tomo, sino, rank, dev, n_threads=None)
         plan = matrixstore.restrict_plan(gplan, vp, rays)
         hf = matrixstore.build_format(sub_ip, t_ix, t_v, len(vp), len(rays), plan,
                                       config.precision, config.ffactor, exp,
-                                      config.smem_budget, schedule)
+                                      config.smem_budget_effective, schedule)
         hf.cta_rows = np.where(hf.cta_rows >= 0, hf.cta_rows + base, -1).astype(np.int32)
         aparts.append(hf)
         aps.append(vp)
