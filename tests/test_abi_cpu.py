@@ -324,3 +324,35 @@ def test_exchange_kernels_accept_empty_lists():
     assert L.xct_gather_rows(None, 0, None, 0, 16, 16, 0, None, None) == 0
     assert L.xct_accumulate_rows(None, 0, None, None, 0, 16, 16, 0, None) == 0
     assert L.xct_gather_rows(None, 10, None, 5, 16, 16, 0, None, None) != 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_format_builder_random_matrices(seed, monkeypatch):
+    """Randomized builder check: ragged and empty rows, repeated columns,
+    random staging keys, tiny capacities (many load groups), one or grouped
+    rows, strict or compressed bank schedule -- every row's (column, value)
+    multiset survives exactly."""
+    rng = np.random.default_rng(seed)
+    n_rows, n_cols = int(rng.integers(1, 300)), int(rng.integers(1, 200))
+    lens = rng.integers(0, 40, n_rows) * (rng.random(n_rows) > 0.1)
+    ip = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ix = rng.integers(0, n_cols, int(ip[-1])).astype(np.int32)
+    v = rng.random(int(ip[-1])) + 0.01
+    keys = rng.integers(0, 7, n_cols).astype(np.int32)
+    prec = ["single", "mixed"][seed % 2]
+    G = [1, 2, 4][seed % 3]
+    compress = bool(seed // 3)
+    monkeypatch.setenv("XCT_SCHED_COMPRESS", "1" if compress else "0")
+    L = matrixstore.lanes_for(16, prec)
+    plan = matrixstore.row_block_plan(n_rows, n_cols, 32 // L * G, 2, keys=keys, row_group=G)
+    rec = matrixstore.f_dev_for(16, prec) * matrixstore.element_bytes(prec)
+    max_key = int(np.bincount(keys).max())
+    budget = 2 * rec * max(max_key, 24)             # a few keys per load group
+    info, a, rows, _ = export(ip, ix, v, n_rows, n_cols, plan, prec, 16, budget=budget,
+                              schedule=True)
+    assert info.nnz == ip[-1] and info.n_groups >= 1
+    seqs = replay_grouped(info, a, rows, n_rows) if G > 1 else replay(info, a, rows, n_rows)
+    sd = matrixstore.storage_dtype(prec)
+    for r in range(n_rows):
+        want = sorted((int(c), float(sd(x))) for c, x in zip(ix[ip[r]:ip[r + 1]], v[ip[r]:ip[r + 1]]))
+        assert sorted(seqs[r]) == want, (seed, r)
