@@ -44,6 +44,8 @@ CONFIGS = {
                 desc="1024x1024, 1024 angles, 256 slices per GPU, FP16 storage"),
     "c5": dict(n=2048, k=2048, slices=1024, precision="mixed", iters=30, strong=True,
                desc="2048x2048, 2048 angles, 1024 slices total, FP16 storage"),
+    "c4": dict(n=2048, k=2048, slices=1024, precision="single", iters=30, strong=True,
+               desc="2048x2048, 2048 angles, 1024 slices total, FP32 (domain-partitioned)"),
     "c3": dict(n=1024, k=1024, slices=2048, precision="single", iters=50, strong=True,
                desc="1024x1024, 1024 angles, 2048 slices total, slice batch, FP32"),
 }
