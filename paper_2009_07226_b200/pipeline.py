@@ -25,7 +25,7 @@ from dataclasses import dataclass, replace
 
 import numpy as np
 
-from . import _lib, engine, hilbert, matrixstore
+from . import _lib, comm, engine, hilbert, matrixstore
 from .geometry import ScanGeometry, SystemMatrix, build_system_matrix, device
 from .matrixstore import NormalizationState
 
@@ -71,8 +71,9 @@ class SystemConfig:
                      projection format is built per chunk of views, the back
                      projection per band of voxels, from Siddon regenerated
                      on the device ("auto": streamed above STREAM_NNZ).
-    ``topology`` and ``comm_strategy`` are accepted for API compatibility;
-    on one NVSwitch box the exchange has a single level.
+    ``topology`` and ``comm_strategy`` select the simulated cluster and
+    planner of ``volume_reports()`` (byte accounting, `comm.py`); on one
+    NVSwitch box the executed exchange has a single level.
     """
 
     precision: str = "double"
@@ -436,20 +437,40 @@ class AssembledSystem:
         return engine.kernel_counters(self.forward.blocks)
 
     def volume_reports(self) -> dict:
-        """Exchange volumes (elements x F x bytes) of the direct plan."""
-        out = {}
-        eb = matrixstore.element_bytes(self.config.precision)
-        for name, side in (("projection", self.forward), ("backprojection", self.adjoint)):
-            if side.footprints[0] is None:
-                out[name] = {"direct_bytes": 0, "ranks": 1}
-                continue
-            owner = np.empty(side.num_outputs, np.int64)
-            for q, own in enumerate(side.ownership):
-                owner[own] = q
-            off = sum(int(np.count_nonzero(owner[fp] != s)) for s, fp in enumerate(side.footprints))
-            out[name] = {"direct_bytes": off * self.config.ffactor * eb,
-                         "ranks": len(side.blocks)}
-        return out
+        """Per-level exchange byte accounting, `comm.VolumeReport` per side,
+        equal to the reference's (src/pipeline.py:115-124, :192-194): the
+        planner named by ``comm_strategy`` over ``topology`` (default: the
+        reference's 4 x 2 x 3 cluster).  Computed on first call, not at
+        assembly, because the simulated placement may not fit a P_b that the
+        B200 slice batch runs (the reference raises then, here this call does)."""
+        if getattr(self, "_volume_reports", None) is None:
+            cfg = self.config
+            topo = cfg.topology if cfg.topology is not None else comm.default_topology()
+            placement = comm.map_partitions(cfg.p_b, cfg.p_d, topo)
+            planner = (comm.plan_hierarchical if cfg.comm_strategy == "hierarchical"
+                       else comm.plan_direct)
+            eb = matrixstore.element_bytes(cfg.precision)
+            out = {}
+            for name, side in (("projection", self.forward), ("backprojection", self.adjoint)):
+                fps = {p: (fp if fp is not None else self._nonempty_outputs(name))
+                       for p, fp in enumerate(side.footprints)}
+                own = {q: np.asarray(o) for q, o in enumerate(side.ownership)}
+                out[name] = planner(fps, own, placement, ffactor=cfg.ffactor,
+                                    elem_bytes=eb)[1]
+            self._volume_reports = out
+        return self._volume_reports
+
+    def _nonempty_outputs(self, name) -> np.ndarray:
+        """P_d = 1 footprint: output elements with at least one entry
+        (src/matrixstore.py:130-148 drops empty rows / untouched columns)."""
+        m = self.matrix
+        n_rows, n_cols = int(m.num_rows), int(m.num_cols)
+        ip, ix = getattr(m, "indptr", None), getattr(m, "indices", None)
+        if ip is None or ix is None:        # streamed build: no host CSR kept
+            return np.arange(n_rows if name == "projection" else n_cols)
+        if name == "projection":
+            return np.flatnonzero(np.diff(np.asarray(ip)) > 0)
+        return np.unique(np.asarray(ix))
 
     def hbm_bytes(self) -> int:
         return sum(b.hbm_bytes() for s in (self.forward, self.adjoint) for b in s.blocks)
