@@ -158,6 +158,7 @@ class _DistSide:
         self.num_inputs, self.num_outputs = len(in_ids), len(own_ids)
         self.n_fp = len(fp_ids)
         self.rank, self.peers = rank, len(fp_of)
+        self.footprints, self.ownership = fp_of, own_of   # all ranks' (volume_reports)
         t = lambda a: torch.as_tensor(np.asarray(a, np.int32), device=dev)
         owner = {}
         # positions of each peer's owned elements inside my footprint (send)
@@ -396,6 +397,24 @@ class DomainPartitionedSystem:
 
     def hbm_bytes(self) -> int:
         return self.forward.block.hbm_bytes() + self.adjoint.block.hbm_bytes()
+
+    def volume_reports(self) -> dict:
+        """Per-level byte accounting of this partition's exchange, the
+        reference's `VolumeReport` per side (src/pipeline.py:192-194) with
+        P_d = world size, planned over ``config.topology`` (comm.py).  Every
+        rank holds all footprints, so no collective is needed."""
+        from . import comm
+        cfg = self.config
+        topo = cfg.topology if cfg.topology is not None else comm.default_topology()
+        placement = comm.map_partitions(1, self.world, topo)
+        planner = (comm.plan_hierarchical if cfg.comm_strategy == "hierarchical"
+                   else comm.plan_direct)
+        eb = matrixstore.element_bytes(cfg.precision)
+        return {name: planner(dict(enumerate(side.footprints)),
+                              dict(enumerate(side.ownership)), placement,
+                              ffactor=cfg.ffactor, elem_bytes=eb)[1]
+                for name, side in (("projection", self.forward),
+                                   ("backprojection", self.adjoint))}
 
     def gather_x(self, x_local):
         """Assemble the full (num_cols, S) estimate on every rank (small

@@ -45,6 +45,11 @@ def main(out_path, n=64, k=96, slices=5):
                 import xct_oracle as O
                 og = O.make_geom(k, slices, n)
                 ora = O.cgls(O.Operator(O.system_matrix(og), og, prec, 4, p_d=ws), y, 6, prec)
+                if prec == "single" and order == "reference":
+                    from dataclasses import asdict
+                    vr, ve = dps.volume_reports(), emu.volume_reports()
+                    report["volume_reports_equal"] = all(
+                        asdict(vr[s]) == asdict(ve[s]) for s in ("projection", "backprojection"))
                 report[f"{prec}_{order}"] = dict(
                     vs_oracle=rel(x, ora["x"]),
                     vs_emulation=rel(x, ref.x), equal_emulation=bool(np.array_equal(x, ref.x)),
