@@ -100,9 +100,28 @@ def test_cli_errors_and_exit_codes(workdir, capsys):
     # role mismatch is a usage error before any device work
     assert main(["recon", "--in", "t.xct", "--geometry", "24,1,16", "--iters", "2",
                  "--out", "r.xct"]) == 2
-    assert main(["plan", "--geometry", "96,1,64", "--report", "p.csv"]) == 2
+    # no P_d fits a cap below the stage buffers (src/cli.py:108-110)
+    assert main(["plan", "--geometry", "96,1,64", "--mem-cap", "1000", "--report", "p.csv"]) == 2
 
 
 def test_slice_groups_rule():
     assert slice_groups(10, 3) == O.slice_groups(10, 3)
     assert slice_groups(3, 8) == [(0, 1), (1, 2), (2, 3)]
+
+
+PLAN = Path(__file__).resolve().parent / "golden" / "plan"
+PLAN_ARGS = {       # tests/golden/make_golden_plan.py, run with the reference CLI
+    "whatif_c4": ["--geometry", "2048,1024,2048"],
+    "whatif_nofit": ["--geometry", "96,1,64", "--pd", "30"],
+    "whatif_cap": ["--geometry", "1024,256,1024", "--precision", "mixed",
+                   "--mem-cap", "3000000000", "--ffactor", "8"],
+}
+
+
+@pytest.mark.parametrize("name", sorted(PLAN_ARGS))
+def test_plan_whatif_matches_reference(workdir, capsys, name):
+    """Analytic what-if path of `xct plan`: same P_d/P_b choice, memory model,
+    stdout and CSV bytes as the reference CLI."""
+    assert main(["plan", *PLAN_ARGS[name], "--report", f"{name}.csv"]) == 0
+    assert Path(f"{name}.csv").read_bytes() == (PLAN / f"{name}.csv").read_bytes()
+    assert capsys.readouterr().out == (PLAN / f"{name}.out").read_text()

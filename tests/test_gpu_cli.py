@@ -116,3 +116,23 @@ def test_bench_sweep(workdir):
     ai = [float(l.split(",")[4]) for l in lines[1:]]
     assert all(b > a for a, b in zip(ai, ai[1:]))
     assert int(lines[1].split(",")[2]) == 2 * int(lines[1].split(",")[1])
+
+
+PLAN = Path(__file__).resolve().parent / "golden" / "plan"
+
+
+@pytest.mark.parametrize("name,args", [
+    ("desk_pd6", ["--geometry", "96,1,64", "--pd", "6", "--precision", "mixed",
+                  "--ffactor", "4"]),
+    ("desk_auto_topo", ["--geometry", "60,3,40", "--mem-cap", "150000", "--stage-capacity",
+                        "16384", "--block-partitions", "2", "--topology", "TOPO",
+                        "--precision", "single"]),
+])
+def test_plan_desk_report_matches_reference(workdir, capsys, name, args):
+    """Desk path of `xct plan`: the per-level communication report of the
+    operator assembled on the GPU equals the reference CLI's CSV and stdout
+    byte for byte (tests/golden/make_golden_plan.py)."""
+    args = [str(PLAN / "topo.txt") if a == "TOPO" else a for a in args]
+    assert main(["plan", *args, "--report", f"{name}.csv"]) == 0
+    assert Path(f"{name}.csv").read_bytes() == (PLAN / f"{name}.csv").read_bytes()
+    assert capsys.readouterr().out == (PLAN / f"{name}.out").read_text()
