@@ -118,3 +118,66 @@ def test_assembled_volume_reports_match_reference(i):
             for p, fp in enumerate(side.footprints):
                 np.testing.assert_array_equal(np.asarray(fp), fps[p])
         check_report(reports[side_name], info["report"])
+
+
+def _random_partition(rng, n_el, p_d):
+    """Random ownership partition and overlapping footprints (some ranks
+    empty, some elements held by many ranks)."""
+    owner = rng.integers(0, p_d, n_el)
+    own = {q: np.flatnonzero(owner == q) for q in range(p_d)}
+    fps = {}
+    for p in range(p_d):
+        dens = rng.choice([0.0, 0.05, 0.3, 0.9])
+        fps[p] = np.flatnonzero(rng.random(n_el) < dens)
+    return fps, own
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_planner_matches_elementwise_oracle(seed):
+    """Random topologies, P_b x P_d placements, ragged/empty footprints:
+    the vectorized planner equals the element-by-element restatement of the
+    reference (oracle.plan_levels) in every transfer list and its order."""
+    import xct_oracle as O
+    rng = np.random.default_rng(seed)
+    topo = comm.Topology(num_nodes=int(rng.integers(2, 5)), sockets_per_node=int(rng.integers(1, 3)),
+                         gpus_per_socket=int(rng.integers(1, 4)))
+    p_d = int(rng.integers(1, topo.gpus_per_node * (topo.num_nodes // 2) + 1))
+    p_b = max(1, topo.num_nodes // -(-p_d // topo.gpus_per_node))
+    placement = comm.map_partitions(p_b, p_d, topo)
+    assert list(placement.slots) == O.placement_slots(p_b, p_d, topo.num_nodes,
+                                                      topo.sockets_per_node, topo.gpus_per_socket)
+    fps, own = _random_partition(rng, int(rng.integers(1, 400)), p_d)
+    for hier in (False, True):
+        planner = comm.plan_hierarchical if hier else comm.plan_direct
+        plan, rep = planner(fps, own, placement, ffactor=3, elem_bytes=2)
+        want, retained = O.plan_levels({p: f.tolist() for p, f in fps.items()},
+                                       {q: o.tolist() for q, o in own.items()},
+                                       placement.slots, topo.sockets_per_node, hier)
+        for lv, (name, t) in zip(plan.levels, want):
+            assert lv.level == name
+            got = {k: v.tolist() for k, v in lv.transfers.items() if k[0] != k[1]}
+            assert list(got) == list(t) and got == t, name
+            assert lv.volume_elements() == sum(len(v) for v in t.values())
+        assert [b // 6 for b in rep.retained_bytes] == retained
+
+
+@pytest.mark.parametrize("i", range(len(CASES)))
+def test_oracle_planner_pinned_to_reference(i):
+    """The element-by-element oracle itself reproduces the reference's
+    golden transfer lists (pins the oracle, tests/golden/comm_plans.npz)."""
+    import xct_oracle as O
+    case = CASES[i]
+    topo = TOPOS[case["topology"]]
+    pl = comm.map_partitions(case["p_b"], case["p_d"], topo)
+    for side in SIDE_NAMES:
+        info = case["sides"][side]
+        key, fps, own = _inputs(i, side, info)
+        want, _ = O.plan_levels({p: f.tolist() for p, f in fps.items()},
+                                {q: o.tolist() for q, o in own.items()},
+                                list(pl.slots), topo.sockets_per_node,
+                                case["strategy"] == "hierarchical")
+        for name, t in want:
+            pairs = [tuple(p) for p in Z[f"{key}_{name}_pairs"].tolist()]
+            ref = {pr: Z[f"{key}_{name}_t{j}"].tolist() for j, pr in enumerate(pairs)
+                   if pr[0] != pr[1]}
+            assert list(ref) == list(t) and ref == t, (side, name)
