@@ -10,11 +10,20 @@ SpMM kernel against measured HBM bandwidth, the CPU baseline (the oracle
 port on an angle subset of the same geometry, extrapolated) and an
 end-to-end number through the public API (cgls_solve on host arrays).
 
-Multi-GPU (torchrun): slice-batch partitioning P_b = N (src/cli.py:158-200):
-each rank reconstructs its own slice group of the same geometry, no
-data-path collective; timing is max over ranks ("scaling": "weak").
+Default workload: BASELINE.json's metric shape, config c5 (2048^2 image,
+2048 views, 1024 slices, FP16 storage with FP32 accumulation) on one GPU.
+The line also carries in-run checks tying the number to a verified result:
+adjointness <A x, y> = <x, A^T y> of the timed fast path on one F-chunk,
+a non-increasing residual, and the FP16 residual curve against an FP32 CGLS
+on a 16-slice subset run through an independent matrix-free FP32 Siddon
+operator (K11).
 
-  python bench.py [--config c2] [--steps K] [--warmup W] [--impl b200|reference]
+Multi-GPU (torchrun): slice-batch partitioning P_b = N (src/cli.py:158-200)
+by default -- each rank reconstructs its own slice group of the same
+geometry, no data-path collective -- or image-domain tiles with the NCCL
+partial-result exchange (--partition domain); timing is max over ranks.
+
+  python bench.py [--config c5] [--steps K] [--warmup W] [--impl b200|reference]
 """
 
 from __future__ import annotations
@@ -126,52 +135,70 @@ def make_problem(cfg, slices):
     return g, geometry.project_f64(g, ph.astype(np.float64))     # (rays, 1)
 
 
-def cpu_baseline(cfg, slices, sample_angles=16, sample_slices=16):
-    """The oracle port timed on an angle subset of the same geometry
-    (BASELINE.md §3): K' views and S' slices, one forward + one back
-    projection + the CG vector updates, extrapolated by (K/K')(S/S')."""
+# CPU sample of the workload (BASELINE.md / SURVEY.md §8(d)(ii)): K' views
+# spread evenly over [0, pi) are bit-identical to every (K/K')-th view of
+# the full geometry when K/K' is a power of two (angles = i * pi / K), so the
+# sample's entries per view are representative of the whole operator.
+SAMPLE_VIEWS, SAMPLE_SLICES = 8, 16
+
+
+def _cpu_sample(cfg, sample_views=SAMPLE_VIEWS, sample_slices=SAMPLE_SLICES):
+    """Oracle port of the reference CPU path (oracle/xct_oracle.py, the
+    restatement of src/pipeline.py + src/solver.py) on the view/slice
+    sample: Shepp-Logan y = A x (src/geometry.py:327-367) and the staged
+    operator (the reference's assembly, untimed)."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import xct_oracle as O
     K, N = cfg["k"], cfg["n"]
-    kp, sp = min(sample_angles, K), min(sample_slices, slices)
-    g = O.make_geom(kp, sp, N, 0.0, kp * math.pi / K)
-    t0 = time.perf_counter()
+    kp, sp = min(sample_views, K), sample_slices
+    if K % kp or (K // kp) & (K // kp - 1):
+        raise ValueError("the view sample must divide K by a power of two")
+    g = O.make_geom(kp, sp, N)
     A = O.system_matrix(g)
-    t_build = time.perf_counter() - t0
+    y = O.measure(A, O.phantom("shepp-logan-like", N, sp))
     op = O.Operator(A, g, cfg["precision"], 16)
-    rng = np.random.default_rng(0)
-    x = rng.random((A.num_cols, sp)).astype(np.float32)
-    yv = rng.random((A.num_rows, sp)).astype(np.float32)
-    op.forward(x)
-    op.adjoint(yv)                         # table construction (= assembly) untimed
-    t0 = time.perf_counter()
-    q, _ = op.forward(x)
-    s, _ = op.adjoint(yv)
-    a = np.float32(0.5)
-    _ = x + a * x
-    _ = yv - a * yv
-    _ = x + a * x
-    t_iter = time.perf_counter() - t0
-    scale = (K / kp) * (slices / sp)
-    return dict(t_iter_sample=t_iter, t_iter_extrap=t_iter * scale, nnz_sample=A.nnz,
-                t_build_sample=t_build, kp=kp, sp=sp, scale=scale)
+    op.adjoint(y.astype(np.float32))          # staging tables built (= assembly), untimed
+    op.forward(np.zeros((A.num_cols, sp), np.float32))
+    return O, op, y, dict(kp=kp, sp=sp, nnz_sample=A.nnz, scale=(K / kp))
+
+
+def cpu_baseline(cfg, slices, iters=2):
+    """One host core: the oracle's CGLS iterations (projection, back
+    projection, dots, normalize/store -- the whole reference iteration,
+    src/solver.py:160-192) on the sample; per-iteration time extrapolated
+    by (K/K') views x (S/S') slices."""
+    O, op, y, info = _cpu_sample(cfg)
+    r = O.cgls(op, y, iters, cfg["precision"])
+    t = statistics.median(r["iteration_seconds"])
+    info.update(t_iter_sample=t, iters=len(r["iteration_seconds"]),
+                t_iter_extrap=t * info["scale"] * (slices / info["sp"]))
+    return info
 
 
 def _reference_worker(job):
-    """One host core's share of the reference arm: the oracle port's CGLS
-    iteration on the angle/slice sample, warmup + steps times."""
-    cfg, total, n = job
+    """One host core's share of the reference arm: build the sample once,
+    then time `n` CGLS iterations of it."""
+    cfg, n = job
     for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[k] = "1"
-    return [cpu_baseline(cfg, total) for _ in range(n)]
+    if n == 0:
+        return None
+    O, op, y, info = _cpu_sample(cfg)
+    r = O.cgls(op, y, n, cfg["precision"])
+    info["times"] = r["iteration_seconds"]
+    return info
 
 
 def run_reference_arm(args, cfg, ws, rank):
     """--impl reference: the reference CPU path (the oracle port of
-    src/engine.py + src/solver.py) on all host cores.  The reference runs
-    one process per slice group (P_b, src/cli.py:158-200) and each group is
-    independent, so every core times the same bounded sample (an exact
-    angle subset) and the cores' rates add up."""
+    src/engine.py + src/solver.py; the reference is pure Python with no
+    build, so there is no oracle/_ref) on every host core.  The reference
+    solves slice groups independently (P_b, src/cli.py:158-200), so each
+    core runs its own sample problem; the W + K step iterations are spread
+    over the cores (each core times its share after building its sample),
+    and the cores' iteration rates add up.  Per-step work: one CGLS
+    iteration over the view/slice sample, extrapolated to the full
+    workload."""
     if rank != 0:
         return
     import multiprocessing as mp
@@ -181,14 +208,18 @@ def run_reference_arm(args, cfg, ws, rank):
     except AttributeError:
         cores = os.cpu_count() or 1
     n = args.warmup + args.steps
+    per = [n // cores + (1 if i < n % cores else 0) for i in range(cores)]
+    per = [max(1, p) for p in per]                     # every core does work
     with mp.get_context("fork").Pool(cores) as pool:
-        runs = pool.map(_reference_worker, [(cfg, total, n)] * cores)
-    r = runs[0][-1]
-    nnz_full = int(round(r["nnz_sample"] * cfg["k"] / r["kp"]))
-    # per core: median extrapolated time of one full-workload iteration;
-    # all cores together finish one iteration in 1 / sum(1 / t_core)
-    t_core = [statistics.median([x["t_iter_extrap"] for x in run[args.warmup:]]) for run in runs]
-    t = 1.0 / sum(1.0 / x for x in t_core)
+        runs = pool.map(_reference_worker, [(cfg, p) for p in per])
+    info = runs[0]
+    # a core's iterations after the first are steady state (the first of
+    # each core pays cold caches); cores ran concurrently
+    t_core = [statistics.median(r["times"][1:] if len(r["times"]) > 1 else r["times"])
+              for r in runs]
+    t_sample = 1.0 / sum(1.0 / t for t in t_core)      # all cores together
+    t = t_sample * info["scale"] * (total / info["sp"])
+    nnz_full = info["nnz_sample"] * info["scale"]
     gflops = 4.0 * nnz_full * total / t / 1e9
     line = {"impl": "reference", "metric": metric_name(cfg), "value": gflops, "unit": "GFLOPS",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -198,11 +229,13 @@ def run_reference_arm(args, cfg, ws, rank):
             "data": "synthetic", "config": config_block(cfg, ws),
             "cg_s_per_iter": t,
             "cpu_baseline": {"value": gflops, "unit": "GFLOPS", "cores": cores, "kind": "port",
-                             "sample": f"oracle port on {cores} host cores (one slice group "
-                                       f"per core), each: views 0..{r['kp'] - 1} of {cfg['k']} "
-                                       f"(bit-exact angle subset), {r['sp']} slices, one CGLS "
-                                       f"iteration, extrapolated x{r['scale']:.0f}",
-                             "per_core_s_per_iter": t_core},
+                             "sample": f"oracle port on {cores} host cores (one sample problem "
+                                       f"per core, {n} timed CGLS iterations spread over them): "
+                                       f"{info['kp']} of {cfg['k']} views (every "
+                                       f"{cfg['k'] // info['kp']}th, bit-exact), "
+                                       f"{info['sp']} of {total} slices; EXTRAPOLATED "
+                                       f"x{info['scale'] * total / info['sp']:.0f}",
+                             "per_core_s_per_iter_sample": t_core},
             "e2e": {"value": gflops, "unit": "GFLOPS", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -236,13 +269,102 @@ def config_block(cfg, ws):
             "streamed from HBM every application), no flush needed"}
 
 
+def _fp32_reference_curve(g, y16, iters):
+    """CGLS in FP32 with the reference's scalar/cast sequence (f64 dots,
+    alpha/beta cast to f32, multiply-then-add updates; src/solver.py:129-196)
+    over the independent matrix-free FP32 operator (K11).  Verification
+    only: the vector updates are plain torch ops."""
+    import torch
+    from paper_2009_07226_b200 import geometry
+    A = lambda v: geometry.project_matrix_free_f32(g, v)
+    At = lambda v: geometry.project_matrix_free_f32(g, v, adjoint=True)
+    dot = lambda a, b: float(torch.sum(a.double() * b.double()))
+    Y = y16.double()
+    ynorm = math.sqrt(dot(Y, Y))
+    x = torch.zeros((g.num_voxels, 16), dtype=torch.float32, device=y16.device)
+    r = y16.clone()
+    s = At(r)
+    p = s.clone()
+    gam = gam0 = dot(s, s)
+    curve = []
+    for _ in range(iters):
+        q = A(p)
+        al = np.float32(gam / dot(q, q))
+        x = x + (p * float(al))
+        r = r - (q * float(al))
+        s = At(r)
+        gn = dot(s, s)
+        be = np.float32(gn / gam)
+        gam = gn
+        p = s + (p * float(be))
+        curve.append(math.sqrt(dot(r, r)) / ynorm)
+    return curve, gam0
+
+
+def run_checks(args, cfg, g, system, y1, history, dev):
+    """Full-size checks of the timed fast path:
+    adjointness on one F-chunk, a non-increasing residual over the timed
+    run, and the residual curve against FP32 on a 16-slice subset (every
+    phantom slice is identical, so the subset's curve is the run's)."""
+    import torch
+    out = {}
+    t0 = time.perf_counter()
+    gen = torch.Generator(device=dev).manual_seed(1)
+    xr = torch.rand((g.num_voxels, 16), generator=gen, device=dev, dtype=torch.float32)
+    yr = torch.rand((g.num_rays, 16), generator=gen, device=dev, dtype=torch.float32)
+    ax, _ = system.apply_forward(xr)
+    aty, _ = system.apply_adjoint(yr)
+    lhs = float(torch.sum(ax.double() * yr.double()))
+    rhs = float(torch.sum(xr.double() * aty.double()))
+    # the same projection through the independent FP32 operator
+    from paper_2009_07226_b200 import geometry
+    ax32 = geometry.project_matrix_free_f32(g, xr)
+    fwd_rel = float(torch.linalg.vector_norm((ax - ax32).double()) /
+                    torch.linalg.vector_norm(ax32.double()))
+    del ax, aty, ax32
+    tol_adj = 2e-3 if cfg["precision"] in ("half", "mixed") else 1e-5
+    out["adjointness"] = {"lhs": lhs, "rhs": rhs, "rel_diff": abs(lhs - rhs) / abs(rhs),
+                          "tol": tol_adj, "ok": abs(lhs - rhs) <= tol_adj * abs(rhs),
+                          "what": "<A x, y> vs <x, A^T y>, random x, y in [0,1), one F-chunk "
+                                  "of 16 slices, timed precision and order"}
+    tol_fwd = 2e-3 if cfg["precision"] in ("half", "mixed") else 1e-5
+    out["forward_vs_fp32_matrix_free"] = {"rel_l2": fwd_rel, "tol": tol_fwd,
+                                          "ok": fwd_rel <= tol_fwd}
+    h = np.asarray(history)
+    worst = float(np.max(h[1:] / h[:-1] - 1.0)) if len(h) > 1 else 0.0
+    out["residual_monotone"] = {"iterations": len(h), "max_rel_increase": worst,
+                                "tol": 1e-3, "ok": worst <= 1e-3,
+                                "first": float(h[0]) if len(h) else None,
+                                "last": float(h[-1]) if len(h) else None}
+    n = min(args.check_iters, len(h))
+    if n:
+        y16 = torch.from_numpy(np.ascontiguousarray(y1, np.float32)).to(dev).expand(
+            g.num_rays, 16).contiguous()
+        ref, _ = _fp32_reference_curve(g, y16, n)
+        dev_rel = np.abs(h[:n] / np.asarray(ref) - 1.0)
+        # tolerance: FP16 storage tracks FP32 within 2% per iteration
+        # (SURVEY.md §8(c)); the reference's own mixed-vs-single gap is
+        # bounded by 3x at iteration 24 (tests/test_solver.py:137-148)
+        out["residual_curve_vs_fp32"] = {
+            "iterations": n, "slices": 16, "fp32_curve": [float(v) for v in ref],
+            "run_curve": [float(v) for v in h[:n]],
+            "max_rel_dev": float(dev_rel.max()), "tol": 0.02,
+            "ok": bool(dev_rel.max() <= 0.02),
+            "fp32_operator": "matrix-free Siddon, FP32 (K11 xct_siddon_project_f32)"}
+    out["seconds"] = time.perf_counter() - t0
+    out["ok"] = all(v.get("ok", True) for v in out.values() if isinstance(v, dict))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--no-checks", action="store_true")
+    ap.add_argument("--check-iters", type=int, default=10)
     ap.add_argument("--precision", default=None)
     ap.add_argument("--order", default="native")
     ap.add_argument("--no-e2e", action="store_true")
@@ -307,13 +429,15 @@ def main():
               torch.empty((g.num_rays, 1), dtype=torch.float64, device=dev))
         dist.broadcast(yt, src=0)
         y1 = yt.cpu().numpy()
-    y = np.broadcast_to(y1, (g.num_rays, S))      # identical phantom slices
+    # identical phantom slices: a zero-stride device view, streamed into the
+    # solver one block of rows at a time (no (rays, S) float64 copy anywhere)
+    y_dev = torch.from_numpy(np.ascontiguousarray(y1)).to(dev).expand(g.num_rays, S)
     torch.cuda.synchronize()
     t_assemble = time.perf_counter() - t0 - t_matrix
     nnz = system.matrix.nnz if not domain else int(round(_global_nnz(system)))
 
     W, K = max(args.warmup, 0), max(args.steps, 1)
-    run = solver.CGLSRun(system, y, solver.SolveConfig(max_iters=W + K + 1,
+    run = solver.CGLSRun(system, y_dev, solver.SolveConfig(max_iters=W + K + 1,
                                                        precision=cfg["precision"]))
     run.start()
     for _ in range(W):
@@ -374,13 +498,23 @@ def main():
     if tf.exists() and ws == 1:     # the ncu capture is of the one-GPU launch
         traffic = json.loads(tf.read_text()).get("bytes_per_launch")
 
-    # end to end through the public API: host y in (pinned), host x out
+    history = list(run.result.residual_history)
+    del run
+    torch.cuda.empty_cache()
+
+    # in-run checks of the timed configuration (rank 0's operator)
+    checks = None
+    if not args.no_checks and not domain:
+        checks = run_checks(args, cfg, g, system, y1, history, dev)
+
+    # end to end through the public API: host float32 y in (pinned), host
+    # float64 x out (src/solver.py:129-196), copies inside the timed region
     e2e = None
     if not args.no_e2e:
         iters = args.e2e_iters or min(cfg["iters"], 10)
-        y_host = torch.from_numpy(np.ascontiguousarray(y)).pin_memory()
-        del run
-        torch.cuda.empty_cache()
+        n_loc = getattr(system, "local_rows", g.num_rays) if domain else g.num_rays
+        y_host = torch.empty((g.num_rays, S), dtype=torch.float32, pin_memory=True)
+        y_host.copy_(torch.from_numpy(y1.astype(np.float32)).expand(g.num_rays, S))
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -395,19 +529,22 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
         e2e = {"value": 4.0 * nnz * S_total * res.iterations / t_e2e / 1e9, "unit": "GFLOPS",
-               "h2d_bytes_per_step": int(y_host.numel() * 8),
+               "h2d_bytes_per_step": int(n_loc * S * 4),
                "d2h_bytes_per_step": int(x_host.numel() * 8),
-               "step": f"one cgls_solve({iters} iterations) call with host arrays",
+               "step": f"one cgls_solve({iters} iterations) call: pinned host float32 y "
+                       f"in, host float64 x out",
                "s_per_call": t_e2e, "iterations": res.iterations}
+        del x_host, res, y_host
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         r = cpu_baseline(cfg, S)
         cpu_gflops = flops_iter / r["t_iter_extrap"] / 1e9
         cpu = {"value": cpu_gflops, "unit": "GFLOPS", "cores": 1, "kind": "port",
-               "sample": f"oracle port, views 0..{r['kp'] - 1} of {cfg['k']} (bit-exact angle "
-                         f"subset), {r['sp']} of {S} slices, one CGLS iteration "
-                         f"({r['t_iter_sample']:.2f} s), extrapolated x{r['scale']:.0f}",
+               "sample": f"oracle port on 1 core: {r['iters']} CGLS iterations over "
+                         f"{r['kp']} of {cfg['k']} views (every {cfg['k'] // r['kp']}th, "
+                         f"bit-exact) x {r['sp']} of {S} slices, {r['t_iter_sample']:.2f} s "
+                         f"per iteration; EXTRAPOLATED x{r['scale'] * S / r['sp']:.0f}",
                "cg_s_per_iter": r["t_iter_extrap"]}
 
     if rank == 0:
@@ -431,7 +568,7 @@ def main():
                          "bytes_model": "nnz*(2+b_x)*ceil(S/16) + (rays+voxels)*S*b_x"},
             "clocks": clocks.summary(),
             "gpu_launches": launches,
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "checks": checks,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

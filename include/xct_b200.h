@@ -59,6 +59,17 @@ int xct_siddon_fill(const double* d_cos, const double* d_sin, int k0, int k1,
                     const int64_t* d_rowptr /* [(k1-k0)*n_det+1], relative */,
                     int32_t* d_indices, double* d_values, void* stream);
 
+/* K11  matrix-free FP32 projector over one chunk of 16 slices: rays
+ * [k0*n_det, k1*n_det) traced on the fly (same Siddon as K1/K2), lengths
+ * rounded to f32, f32 accumulation.  adjoint == 0: d_out[r][16] =
+ * sum_j len_j * d_in[vox_j][16] (rays relative to k0); adjoint != 0:
+ * d_out[vox][16] += len * d_in[r][16] with f32 atomics (caller zeroes
+ * d_out).  An independent single-precision operator (cf. engine.project in
+ * "single" mode, src/engine.py:119-166) for checking the staged path. */
+int xct_siddon_project_f32(const double* d_cos, const double* d_sin, int k0, int k1,
+                           int n_det, int grid_n, double voxel_size, int adjoint,
+                           const float* d_in, float* d_out, void* stream);
+
 /* Column-range restriction of a device CSR for the streamed operator build
  * (the back-projection format is built one band of voxels at a time; cf.
  * matrixstore._restrict_rows, src/matrixstore.py:151-165).  Count pass when
@@ -256,6 +267,22 @@ int xct_unchunk_f64(const void* d_in, int in_dtype, float fin, int64_t n,
 int xct_chunk_from_f64(const double* d_in, int64_t n, int64_t n_slices,
                        int32_t ffactor, int32_t f_dev, int out_dtype,
                        void* d_out, void* stream);
+
+/* Measurements / results in the caller's row-major (n, n_slices) layout,
+ * streamed one block of rows at a time (cgls_solve with host arrays,
+ * src/solver.py:137 and :194-195):
+ * rows_to_chunked: rows [r0, r0+nr) (d_rows = that block, f64 or f32) ->
+ *   chunked work layout (f64 or f32, round to nearest); max|v| and
+ *   max|wd(v)| as f64 bits (atomic max into zeroed slots) and, if d_sumsq,
+ *   the f64 sum of v*v of the block (d_scratch[148*8]);
+ * unchunk_rows_f64: rows [r0, r0+nr) of a chunked vector -> (nr, n_slices) f64. */
+int xct_rows_to_chunked(const void* d_rows, int in_dtype, int64_t r0, int64_t nr, int64_t n,
+                        int64_t n_slices, int32_t ffactor, int32_t f_dev, int out_dtype,
+                        void* d_out, uint64_t* d_max_in, uint64_t* d_max_out,
+                        double* d_scratch, double* d_sumsq, void* stream);
+int xct_unchunk_rows_f64(const void* d_in, int in_dtype, float fin, int64_t n, int64_t r0,
+                         int64_t nr, int64_t n_slices, int32_t ffactor, int32_t f_dev,
+                         double* d_out, void* stream);
 
 /* ---------------------------------------------------------------------------
  * K10  partial-result exchange of the data-partitioned operator

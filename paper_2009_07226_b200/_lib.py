@@ -50,6 +50,7 @@ _SIGS = {
     "xct_last_error": (C.c_char_p, []),
     "xct_siddon_count": (i32, [vp, vp, i32, i32, i32, i32, f64, vp, vp]),
     "xct_siddon_fill": (i32, [vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp]),
+    "xct_siddon_project_f32": (i32, [vp, vp, i32, i32, i32, i32, f64, i32, vp, vp, vp]),
     "xct_csr_filter_cols": (i32, [vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp]),
     "xct_csr_filter_map": (i32, [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]),
     "xct_format_build": (i32, [i64, i64, vp, vp, vp, i64, i64, i64, vp, vp, vp, i64, i32,
@@ -70,6 +71,9 @@ _SIGS = {
     "xct_normalize_chunked": (i32, [vp, i32, f32, i64, i64, i32, vp, i32, vp, vp]),
     "xct_unchunk_f64": (i32, [vp, i32, f32, i64, i64, i32, i32, vp, vp]),
     "xct_chunk_from_f64": (i32, [vp, i64, i64, i32, i32, i32, vp, vp]),
+    "xct_rows_to_chunked": (i32, [vp, i32, i64, i64, i64, i64, i32, i32, i32, vp, vp, vp, vp,
+                                  vp, vp]),
+    "xct_unchunk_rows_f64": (i32, [vp, i32, f32, i64, i64, i64, i64, i32, i32, vp, vp]),
     "xct_gather_rows": (i32, [vp, i64, vp, i64, i64, i32, i32, vp, vp]),
     "xct_accumulate_rows": (i32, [vp, i64, vp, vp, i64, i64, i32, i32, vp]),
     "xct_scale_chunks": (i32, [vp, i64, i64, vp, i32, vp, vp, vp]),
@@ -124,7 +128,9 @@ KERNELS_PER_CALL = {"xct_dot": 2, "xct_sum_f64": 1, "xct_spmm": 1, "xct_maxabs":
                     "xct_normalize_chunked": 1, "xct_unchunk_f64": 1, "xct_chunk_from_f64": 1,
                     "xct_csr_spmm_f64": 1, "xct_siddon_count": 1, "xct_siddon_fill": 1,
                     "xct_csr_filter_cols": 1, "xct_csr_filter_map": 1, "xct_gather_rows": 1,
-                    "xct_accumulate_rows": 1, "xct_scale_chunks": 2}
+                    "xct_accumulate_rows": 1, "xct_scale_chunks": 2,
+                    "xct_rows_to_chunked": 2, "xct_unchunk_rows_f64": 1,
+                    "xct_siddon_project_f32": 1}
 launch_count = [0]
 
 

@@ -302,3 +302,84 @@ extern "C" int xct_csr_filter_map(const int64_t* d_indptr, const int32_t* d_indi
   XCT_CUDA_CHECK_LAUNCH("csr_filter_map");
   return XCT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// K11: matrix-free FP32 projector pair over one chunk of 16 slices -- the
+// same Siddon rays traced on the fly (no stored operator), lengths rounded
+// to f32, accumulation in f32.  An independent implementation of the
+// single-precision operator (cf. engine.project, src/engine.py:119-166, in
+// "single" mode) used to check the staged K6 path at sizes whose FP32
+// staged operator does not fit next to the FP16 one (bench.py in-run
+// checks).  Back projection scatters with vector f32 atomics, so its sums
+// are order-nondeterministic at the last bit.
+namespace {
+constexpr int kMfSlices = 16;
+
+__global__ void siddon_project_f32_kernel(const double* __restrict__ cos_t,
+                                          const double* __restrict__ sin_t, int k0, int k1,
+                                          int n_det, int g, double vox,
+                                          const float4* __restrict__ x, float4* __restrict__ y) {
+  const int64_t n_rays = (int64_t)(k1 - k0) * n_det;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rays;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int k = k0 + (int)(r / n_det), c = (int)(r % n_det);
+    float4 acc[kMfSlices / 4];
+#pragma unroll
+    for (int q = 0; q < kMfSlices / 4; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    trace(cos_t[k], sin_t[k], c, n_det, g, vox, [&](int64_t, int32_t flat, double len) {
+      const float l = (float)len;
+      const float4* xp = x + (int64_t)flat * (kMfSlices / 4);
+#pragma unroll
+      for (int q = 0; q < kMfSlices / 4; ++q) {
+        const float4 v = __ldg(xp + q);
+        acc[q].x = fmaf(v.x, l, acc[q].x);
+        acc[q].y = fmaf(v.y, l, acc[q].y);
+        acc[q].z = fmaf(v.z, l, acc[q].z);
+        acc[q].w = fmaf(v.w, l, acc[q].w);
+      }
+    });
+#pragma unroll
+    for (int q = 0; q < kMfSlices / 4; ++q) y[r * (kMfSlices / 4) + q] = acc[q];
+  }
+}
+
+__global__ void siddon_backproject_f32_kernel(const double* __restrict__ cos_t,
+                                              const double* __restrict__ sin_t, int k0, int k1,
+                                              int n_det, int g, double vox,
+                                              const float4* __restrict__ y, float4* __restrict__ x) {
+  const int64_t n_rays = (int64_t)(k1 - k0) * n_det;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rays;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int k = k0 + (int)(r / n_det), c = (int)(r % n_det);
+    float4 yv[kMfSlices / 4];
+#pragma unroll
+    for (int q = 0; q < kMfSlices / 4; ++q) yv[q] = y[r * (kMfSlices / 4) + q];
+    trace(cos_t[k], sin_t[k], c, n_det, g, vox, [&](int64_t, int32_t flat, double len) {
+      const float l = (float)len;
+      float4* xp = x + (int64_t)flat * (kMfSlices / 4);
+#pragma unroll
+      for (int q = 0; q < kMfSlices / 4; ++q)
+        atomicAdd(xp + q, make_float4(yv[q].x * l, yv[q].y * l, yv[q].z * l, yv[q].w * l));
+    });
+  }
+}
+}  // namespace
+
+extern "C" int xct_siddon_project_f32(const double* d_cos, const double* d_sin, int k0, int k1,
+                                      int n_det, int grid_n, double voxel_size, int adjoint,
+                                      const float* d_in, float* d_out, void* stream) {
+  int st = check_args(d_cos, d_sin, k0, k1, n_det, grid_n, voxel_size);
+  if (st) return st;
+  if (!d_in || !d_out) return xct::fail(XCT_EINVAL, "siddon_project_f32: null vector");
+  const int64_t n = (int64_t)(k1 - k0) * n_det;
+  if (n == 0) return XCT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (adjoint)
+    siddon_backproject_f32_kernel<<<grid_for(n, 128), 128, 0, s>>>(
+        d_cos, d_sin, k0, k1, n_det, grid_n, voxel_size, (const float4*)d_in, (float4*)d_out);
+  else
+    siddon_project_f32_kernel<<<grid_for(n, 128), 128, 0, s>>>(
+        d_cos, d_sin, k0, k1, n_det, grid_n, voxel_size, (const float4*)d_in, (float4*)d_out);
+  XCT_CUDA_CHECK_LAUNCH("siddon_project_f32");
+  return XCT_OK;
+}

@@ -363,6 +363,51 @@ __global__ void unchunk_f64_k(const void* in, int dtype, float fin, int64_t n, i
   }
 }
 
+
+// Row block [r0, r0+nr) of a row-major (n, n_slices) f64/f32 array (the
+// caller's measurements, src/solver.py:137: Y = y.astype(f64)) -> the
+// chunked work layout: out[(c*n + r0+i)*f_dev + jj] = wd(v) (f64, or f32 by
+// round-to-nearest like ndarray.astype(float32)); also max|v| (f64 bits),
+// max|wd(v)| and per-block f64 partial sums of v*v (deterministic order).
+template <typename In, typename Out>
+__global__ void rows_to_chunked_k(const In* __restrict__ in, int64_t r0, int64_t nr, int64_t n,
+                                  int64_t n_slices, int ff, int f_dev, Out* __restrict__ out,
+                                  unsigned long long* max_in, unsigned long long* max_out,
+                                  double* partials) {
+  const int64_t total = nr * n_slices;
+  unsigned long long mi = 0, mo = 0;
+  double sq = 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / n_slices, j = t % n_slices;
+    const double v = (double)in[t];
+    const Out w = (Out)in[t];
+    out[((j / ff) * n + r0 + i) * f_dev + (j % ff)] = w;
+    const unsigned long long bi = abs_bits(v), bo = abs_bits((double)w);
+    mi = bi > mi ? bi : mi;
+    mo = bo > mo ? bo : mo;
+    sq += v * v;
+  }
+  mi = block_max(mi);
+  mo = block_max(mo);
+  sq = block_sum(sq);
+  if (threadIdx.x == 0) {
+    if (max_in && mi) atomicMax(max_in, mi);
+    if (max_out && mo) atomicMax(max_out, mo);
+    if (partials) partials[blockIdx.x] = sq;
+  }
+}
+
+// rows [r0, r0+nr) of a chunked vector -> row-major (nr, n_slices) f64
+__global__ void unchunk_rows_f64_k(const void* in, int dtype, float fin, int64_t n, int64_t r0,
+                                   int64_t nr, int64_t n_slices, int ff, int f_dev, double* out) {
+  const int64_t total = nr * n_slices;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / n_slices, j = t % n_slices;
+    out[t] = load_as_f64(in, dtype, fin, ((j / ff) * n + r0 + i) * f_dev + (j % ff));
+  }
+}
 }  // namespace
 
 extern "C" int xct_chunk_maxabs(const void* d_v, int in_f64, int64_t n, int64_t n_slices,
@@ -716,5 +761,50 @@ extern "C" int xct_scale_chunks(void* d_v, int64_t per_chunk, int64_t n_chunks,
   else scale_chunks_k<float><<<g, kThreads, 0, s>>>((float*)d_v, per_chunk, n_chunks, d_factors, partials);
   if (partials) final_sum_kernel<<<1, 1024, 0, s>>>(partials, g, d_sumsq);
   XCT_CUDA_CHECK_LAUNCH("scale_chunks");
+  return XCT_OK;
+}
+
+extern "C" int xct_rows_to_chunked(const void* d_rows, int in_dtype, int64_t r0, int64_t nr,
+                                   int64_t n, int64_t n_slices, int32_t ffactor, int32_t f_dev,
+                                   int out_dtype, void* d_out, uint64_t* d_max_in,
+                                   uint64_t* d_max_out, double* d_scratch, double* d_sumsq,
+                                   void* stream) {
+  if (!d_rows || !d_out || (in_dtype != 0 && in_dtype != 1) || (out_dtype != 0 && out_dtype != 1) ||
+      ffactor < 1 || f_dev < ffactor || r0 < 0 || nr < 0 || r0 + nr > n)
+    return xct::fail(XCT_EINVAL, "rows_to_chunked: bad argument");
+  const int64_t total = nr * n_slices;
+  if (total == 0) return XCT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int g = blocks_for(total);
+  double* part = d_sumsq ? d_scratch : nullptr;
+  if (d_sumsq && !d_scratch) return xct::fail(XCT_EINVAL, "rows_to_chunked: sumsq needs scratch");
+  auto* mi = (unsigned long long*)d_max_in;
+  auto* mo = (unsigned long long*)d_max_out;
+  if (in_dtype == 0 && out_dtype == 0)
+    rows_to_chunked_k<double, double><<<g, kThreads, 0, s>>>((const double*)d_rows, r0, nr, n,
+        n_slices, ffactor, f_dev, (double*)d_out, mi, mo, part);
+  else if (in_dtype == 0)
+    rows_to_chunked_k<double, float><<<g, kThreads, 0, s>>>((const double*)d_rows, r0, nr, n,
+        n_slices, ffactor, f_dev, (float*)d_out, mi, mo, part);
+  else if (out_dtype == 0)
+    rows_to_chunked_k<float, double><<<g, kThreads, 0, s>>>((const float*)d_rows, r0, nr, n,
+        n_slices, ffactor, f_dev, (double*)d_out, mi, mo, part);
+  else
+    rows_to_chunked_k<float, float><<<g, kThreads, 0, s>>>((const float*)d_rows, r0, nr, n,
+        n_slices, ffactor, f_dev, (float*)d_out, mi, mo, part);
+  if (part) final_sum_kernel<<<1, 1024, 0, s>>>(part, g, d_sumsq);
+  XCT_CUDA_CHECK_LAUNCH("rows_to_chunked");
+  return XCT_OK;
+}
+
+extern "C" int xct_unchunk_rows_f64(const void* d_in, int in_dtype, float fin, int64_t n,
+                                    int64_t r0, int64_t nr, int64_t n_slices, int32_t ffactor,
+                                    int32_t f_dev, double* d_out, void* stream) {
+  if (!d_in || !d_out || r0 < 0 || nr < 0 || r0 + nr > n || ffactor < 1)
+    return xct::fail(XCT_EINVAL, "unchunk_rows_f64: bad argument");
+  if (nr * n_slices == 0) return XCT_OK;
+  unchunk_rows_f64_k<<<blocks_for(nr * n_slices), kThreads, 0, (cudaStream_t)stream>>>(
+      d_in, in_dtype, fin, n, r0, nr, n_slices, ffactor, f_dev, d_out);
+  XCT_CUDA_CHECK_LAUNCH("unchunk_rows_f64");
   return XCT_OK;
 }

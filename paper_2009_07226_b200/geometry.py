@@ -382,3 +382,35 @@ def project_f64(geometry: ScanGeometry, x: np.ndarray, chunk_nnz: float = 4e8) -
                   y.data_ptr(), st)
         out[k0 * n:k1 * n] = y.cpu().numpy()
     return out.reshape(geometry.num_rays) if x.ndim == 1 else out
+
+
+def project_matrix_free_f32(geometry: ScanGeometry, data, adjoint: bool = False):
+    """Matrix-free single-precision projection of one chunk of 16 slices on
+    the device (K11 ``xct_siddon_project_f32``): the Siddon rays are traced
+    on the fly, no operator is stored.  ``data``: CUDA float32 tensor
+    (num_voxels, 16) for the projection, (num_rays, 16) for the back
+    projection (adjoint=True).  An independent FP32 implementation of the
+    operator, used to check the staged path where an FP32 staged operator
+    would not fit (bench.py, 2048^2 x 2048 views)."""
+    import torch
+    if not (isinstance(data, torch.Tensor) and data.is_cuda and data.dtype == torch.float32):
+        raise ValueError("project_matrix_free_f32 expects a CUDA float32 tensor")
+    n_in = geometry.num_rays if adjoint else geometry.num_voxels
+    n_out = geometry.num_voxels if adjoint else geometry.num_rays
+    if tuple(data.shape) != (n_in, 16):
+        raise ValueError(f"expected shape ({n_in}, 16), got {tuple(data.shape)}")
+    dev = data.device
+    key = (geometry, str(dev))
+    tabs = _MF_TABLES.get(key)
+    if tabs is None:
+        tabs = _MF_TABLES[key] = _angle_tables(geometry, dev)
+    cs, sn = tabs
+    x = data.contiguous()
+    out = torch.zeros((n_out, 16), dtype=torch.float32, device=dev)
+    _lib.call("xct_siddon_project_f32", _lib.ptr(cs), _lib.ptr(sn), 0, geometry.num_angles,
+              geometry.num_detector_cols, geometry.grid_n, float(geometry.voxel_size),
+              int(bool(adjoint)), x.data_ptr(), out.data_ptr(), _lib.stream_handle(dev))
+    return out
+
+
+_MF_TABLES: dict = {}

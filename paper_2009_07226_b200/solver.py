@@ -115,6 +115,11 @@ def residual_curve_report(histories: dict) -> str:
     return "\n".join(lines) + "\n"
 
 
+# measurements and results move between the caller's (rows, slices) layout
+# and the device in blocks of rows of about this many bytes
+_ROW_BLOCK_BYTES = 512 << 20
+
+
 class _Vec:
     """A persistent CG vector: payload tensor + dtype code + load factor."""
 
@@ -305,108 +310,114 @@ class CGLSRun:
 
     def start(self) -> bool:
         """Setup and the initial back projection (src/solver.py:141-157).
-        y is streamed one F-chunk of slices at a time (host or device), so
-        no full-size float64/float32 copy of the measurements is ever made
-        on the device: pass 1 reduces max|wd(y)| and ||y||^2, pass 2 writes
-        the stored residual r = store(wd(y))."""
+        Measurements in the caller's row-major layout (host array, pinned or
+        not, or a CUDA tensor; float32 or float64) stream through the device
+        one block of rows at a time into the chunked work layout (K7
+        ``xct_rows_to_chunked``: max|y|, ||y||^2 and wd(y) in one pass), so
+        no full float64 copy of y is ever made on the device."""
         import torch
-        cg, prec, system = self.cg, self.config.precision, self.system
-        S = cg.S
-        y = self.y.reshape(system.num_rows, S)
-        # distributed operators own a subset of the rays and voxels
+        cg, system = self.cg, self.system
+        y = self.y.reshape(system.num_rows, cg.S)
         owned = getattr(system, "row_owned", None)
         n_rows = getattr(system, "local_rows", system.num_rows)
         n_cols = getattr(system, "local_cols", system.num_cols)
-
-        # host measurements that fit comfortably are uploaded once, whole
-        # rows at a time (contiguous, pinned-speed copies); larger ones are
-        # streamed one slice chunk at a time
-        is_host = isinstance(y, np.ndarray) or not y.is_cuda
-        nbytes = n_rows * S * 8
         lap = _Lap(cg.dev)
-        if is_host and nbytes <= min(16 << 30, torch.cuda.mem_get_info(cg.dev)[0] // 4):
-            yd = torch.empty((n_rows, S), dtype=torch.float64, device=cg.dev)
-            rows_per = max(1, (256 << 20) // max(1, S * 8))
-            for r0 in range(0, n_rows, rows_per):
-                r1 = min(n_rows, r0 + rows_per)
-                blk = y[r0:r1] if owned is None else y[owned[r0:r1]]
-                if isinstance(blk, np.ndarray):
-                    blk = torch.from_numpy(np.ascontiguousarray(blk, dtype=np.float64))
-                yd[r0:r1].copy_(blk, non_blocking=True)
-            y, owned = yd, None
-            lap("start: upload y")
-
-        def chunk(c):
-            lo, hi = c * cg.F, min(S, (c + 1) * cg.F)
-            yc = y[:, lo:hi] if owned is None else y[owned, lo:hi]
-            if isinstance(yc, np.ndarray):
-                yc = torch.from_numpy(np.ascontiguousarray(yc, dtype=np.float64))
-            return yc.to(device=cg.dev, dtype=torch.float64).contiguous(), hi - lo
-
-        per = n_rows * cg.f_dev
-        tmp = torch.empty(per, dtype=cg.wdt, device=cg.dev)
-        if cg.reduced:
-            r = _Vec(torch.empty(cg.numel(n_rows), dtype=torch.float16, device=cg.dev), 2, 1.0)
-        else:
-            r = _Vec(torch.empty(cg.numel(n_rows), dtype=cg.wdt, device=cg.dev), cg.code)
-        ybits = torch.zeros(1, dtype=torch.int64, device=cg.dev)
-        rbits = torch.zeros(1, dtype=torch.int64, device=cg.dev)
-        y_sq = 0.0
-        for c in range(cg.n_chunks):
-            yc, w = chunk(c)
-            _lib.call("xct_maxabs", yc.data_ptr(), 0, yc.numel(), 1.0, ybits.data_ptr(), cg.st)
-            _lib.call("xct_dot", yc.data_ptr(), yc.data_ptr(), 0, yc.numel(), 1.0, 1.0,
-                      cg.scratch.data_ptr(), cg.scal.data_ptr(), cg.st)
-            y_sq += float(cg.scal[0].item())
-            dst = tmp if cg.reduced else r.t[c * per:(c + 1) * per]
-            _lib.call("xct_chunk_from_f64", yc.data_ptr(), n_rows, w, cg.F, cg.f_dev, cg.code,
-                      dst.data_ptr(), cg.st)
-            if cg.reduced:
-                _lib.call("xct_maxabs", tmp.data_ptr(), 1, per, 1.0, rbits.data_ptr(), cg.st)
-        lap("start: y norm and store pass 1")
-        cg.comm.max_bits(ybits)
-        if not math.isfinite(float(ybits.cpu().numpy().view(np.float64)[0])):
-            raise SolverDivergence(0, prec, "measurement data contains NaN or Inf")
-        y_sq = cg.comm.sum(y_sq)
-        self.y_norm = math.sqrt(y_sq)
-        if self.y_norm == 0.0:
+        r = self._store_measurements(y, owned, n_rows)
+        lap("start: y upload, norm and store")
+        if r is None:
             self.done = True
             self.x = None
             return False
-        if cg.reduced:
-            cg.comm.max_bits(rbits)
-            peak = float(rbits.cpu().numpy().view(np.float64)[0])
-            r.factor = peak if peak > 0 else 1.0
-            f32 = float(np.float32(r.factor))
-            for c in range(cg.n_chunks):
-                yc, w = chunk(c)
-                _lib.call("xct_chunk_from_f64", yc.data_ptr(), n_rows, w, cg.F, cg.f_dev, 1,
-                          tmp.data_ptr(), cg.st)
-                _lib.call("xct_axpy", tmp.data_ptr(), 1, 1.0, None, 1, 1.0, 0.0, per,
-                          r.t[c * per:(c + 1) * per].data_ptr(), 2, f32, None,
-                          cg.scratch.data_ptr(), None, cg.st)
-        del tmp, y
         self.r = r
         if cg.reduced:
             self.x = _Vec(torch.zeros(cg.numel(n_cols), dtype=torch.float16, device=cg.dev), 2, 1.0)
         else:
             self.x = _Vec(torch.zeros(cg.numel(n_cols), dtype=cg.wdt, device=cg.dev), cg.code)
-        # one output buffer serves q (projection) and s (back projection):
-        # q is dead once r is updated, s is produced after that
-        buf = torch.empty(cg.numel(max(n_rows, n_cols)), dtype=cg.out_dt, device=cg.dev)
-        self.s_buf = buf[:cg.numel(n_cols)]
-        self.q_buf = buf[:cg.numel(n_rows)]
-        lap("start: store pass 2")
         facs, gamma = cg.apply(system.adjoint, self.r, self.s_buf)
         lap("start: first back projection")
         if facs is None:
-            raise SolverDivergence(0, prec, "residual contains NaN or Inf")
+            raise SolverDivergence(0, self.config.precision, "residual contains NaN or Inf")
         self.result.backprojections += 1
         self.result.normalization_factors.append(facs)
         s = self._work(self.s_buf)
         self.p = cg.store(s.t) if cg.reduced else _Vec(s.t.clone(), cg.code)
         self.gamma = self.gamma0 = gamma
         return True
+
+    def _store_measurements(self, y, owned, n_rows):
+        """r = store(wd(y)), ||y|| and the finite check (src/solver.py:137-150).
+        Also allocates the q/s output buffer, which stages wd(y) on the way."""
+        import torch
+        cg, prec = self.cg, self.config.precision
+        S = cg.S
+        n_cols = getattr(self.system, "local_cols", self.system.num_cols)
+        # one output buffer serves q (projection) and s (back projection): q
+        # is dead once r is updated, s is produced after that; before the
+        # first back projection it holds wd(y) for the reduced store
+        buf = torch.empty(cg.numel(max(n_rows, n_cols)), dtype=cg.out_dt, device=cg.dev)
+        self.s_buf = buf[:cg.numel(n_cols)]
+        self.q_buf = buf[:cg.numel(n_rows)]
+        if cg.reduced:
+            work = buf[:cg.numel(n_rows)]
+            if cg.out_dt != cg.wdt:
+                work = torch.empty(cg.numel(n_rows), dtype=cg.wdt, device=cg.dev)
+        else:
+            work = torch.empty(cg.numel(n_rows), dtype=cg.wdt, device=cg.dev)
+        if S % cg.F or cg.f_dev != cg.F:
+            work.zero_()                      # padding slices stay 0
+        ybits = torch.zeros(1, dtype=torch.int64, device=cg.dev)
+        wbits = torch.zeros(1, dtype=torch.int64, device=cg.dev)
+        is_t = isinstance(y, torch.Tensor)
+        if owned is not None:                 # distributed: this rank's rays only
+            idx = torch.as_tensor(np.asarray(owned, np.int64))
+            y = y[idx.to(y.device)] if is_t else np.asarray(y)[np.asarray(owned)]
+        if is_t:
+            src = y if y.dtype in (torch.float32, torch.float64) else y.to(torch.float64)
+            f32_in, on_dev = src.dtype == torch.float32, src.is_cuda
+        else:
+            src = np.asarray(y)
+            if src.dtype not in (np.float32, np.float64):
+                src = src.astype(np.float64)
+            f32_in, on_dev = src.dtype == np.float32, False
+        # blocks of rows: a broadcast (zero-stride) or strided input is only
+        # ever materialized one block at a time
+        rows_per = max(1, _ROW_BLOCK_BYTES // max(1, S * (4 if f32_in else 8)))
+        blocks = [(r0, min(n_rows, r0 + rows_per)) for r0 in range(0, n_rows, rows_per)]
+        sums = torch.zeros(max(len(blocks), 1), dtype=torch.float64, device=cg.dev)
+        stage = None
+        if not on_dev and blocks:
+            stage = torch.empty((min(rows_per, n_rows), S),
+                                dtype=torch.float32 if f32_in else torch.float64, device=cg.dev)
+        for b, (r0, r1) in enumerate(blocks):
+            part = src[r0:r1]
+            if on_dev:
+                blk = part.contiguous()
+            else:
+                blk = stage[:r1 - r0]
+                if isinstance(part, torch.Tensor):
+                    blk.copy_(part, non_blocking=part.is_pinned())
+                else:
+                    _lib.to_device(np.ascontiguousarray(part), blk)
+            _lib.call("xct_rows_to_chunked", blk.data_ptr(), 1 if f32_in else 0, r0, r1 - r0,
+                      n_rows, S, cg.F, cg.f_dev, cg.code, work.data_ptr(), ybits.data_ptr(),
+                      wbits.data_ptr(), cg.scratch.data_ptr(), sums[b:b + 1].data_ptr(), cg.st)
+        y_sq = float(sums.cpu().numpy().sum()) if n_rows else 0.0
+        cg.comm.max_bits(ybits)
+        if not math.isfinite(float(ybits.cpu().numpy().view(np.float64)[0])):
+            raise SolverDivergence(0, prec, "measurement data contains NaN or Inf")
+        self.y_norm = math.sqrt(cg.comm.sum(y_sq))
+        if self.y_norm == 0.0:
+            return None
+        if not cg.reduced:
+            return _Vec(work, cg.code)
+        cg.comm.max_bits(wbits)
+        peak = float(wbits.cpu().numpy().view(np.float64)[0])
+        factor = peak if peak > 0 else 1.0
+        r = _Vec(torch.empty(cg.numel(n_rows), dtype=torch.float16, device=cg.dev), 2, factor)
+        _lib.call("xct_axpy", work.data_ptr(), cg.code, 1.0, None, cg.code, 1.0, 0.0, work.numel(),
+                  r.t.data_ptr(), 2, float(np.float32(factor)), None, cg.scratch.data_ptr(),
+                  None, cg.st)
+        return r
 
     def _work(self, buf) -> _Vec:
         cg = self.cg
@@ -469,19 +480,26 @@ class CGLSRun:
                 out = torch.zeros((n_cols, S), dtype=torch.float64, device=cg.dev)
         else:
             lap = _Lap(cg.dev)
-            xf = torch.empty((n_cols, S), dtype=torch.float64, device=cg.dev)
-            _lib.call("xct_unchunk_f64", self.x.t.data_ptr(), self.x.code,
-                      float(np.float32(self.x.factor)), n_cols, S, cg.F, cg.f_dev,
-                      xf.data_ptr(), cg.st)
+            fx = float(np.float32(self.x.factor))
             if self.is_np or not self.y.is_cuda:
-                # host in -> host out, through pinned staging (a pageable
-                # .cpu() of a 2 GB result takes ~1 s on the B200 host)
+                # host in -> host out: unchunk one block of rows at a time
+                # and copy it through pinned staging into the result (a
+                # whole float64 x on the device would cost C*S*8 bytes)
                 torch.cuda.synchronize(cg.dev)
-                out = _lib.to_host(xf)
+                out = np.empty((n_cols, S), np.float64)
+                per = max(1, _ROW_BLOCK_BYTES // max(1, S * 8))
+                xf = torch.empty((min(per, n_cols), S), dtype=torch.float64, device=cg.dev)
+                for r0 in range(0, n_cols, per):
+                    r1 = min(n_cols, r0 + per)
+                    _lib.call("xct_unchunk_rows_f64", self.x.t.data_ptr(), self.x.code, fx,
+                              n_cols, r0, r1 - r0, S, cg.F, cg.f_dev, xf.data_ptr(), cg.st)
+                    _lib.to_host(xf[:r1 - r0], out=out[r0:r1])
                 if not self.is_np:
                     out = torch.from_numpy(out)
             else:
-                out = xf
+                out = torch.empty((n_cols, S), dtype=torch.float64, device=cg.dev)
+                _lib.call("xct_unchunk_f64", self.x.t.data_ptr(), self.x.code, fx, n_cols, S,
+                          cg.F, cg.f_dev, out.data_ptr(), cg.st)
             lap("finish: x to the caller")
         self.result.x = out[:, 0] if self.squeeze else out
         return self.result
