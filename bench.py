@@ -341,15 +341,20 @@ def run_checks(args, cfg, g, system, y1, history, dev):
         y16 = torch.from_numpy(np.ascontiguousarray(y1, np.float32)).to(dev).expand(
             g.num_rays, 16).contiguous()
         ref, _ = _fp32_reference_curve(g, y16, n)
-        dev_rel = np.abs(h[:n] / np.asarray(ref) - 1.0)
-        # tolerance: FP16 storage tracks FP32 within 2% per iteration
-        # (SURVEY.md §8(c)); the reference's own mixed-vs-single gap is
-        # bounded by 3x at iteration 24 (tests/test_solver.py:137-148)
+        ratio = h[:n] / np.asarray(ref)
+        lead = int(np.argmax(np.abs(ratio - 1.0) > 0.02)) if np.any(np.abs(ratio - 1.0) > 0.02) \
+            else n
+        # FP16 storage tracks FP32 until its quantization floor, then sits
+        # above it: the reference's own mixed/single residual ratio reaches
+        # 1.36 at config 1 and 1.23 at N = K = 256 (tests/golden: c1,
+        # sub256) and its test bounds it by 3 (tests/test_solver.py:137-148);
+        # the check bounds it by 1.5 at every iteration
         out["residual_curve_vs_fp32"] = {
             "iterations": n, "slices": 16, "fp32_curve": [float(v) for v in ref],
             "run_curve": [float(v) for v in h[:n]],
-            "max_rel_dev": float(dev_rel.max()), "tol": 0.02,
-            "ok": bool(dev_rel.max() <= 0.02),
+            "max_ratio": float(ratio.max()), "min_ratio": float(ratio.min()),
+            "leading_iterations_within_2pct": lead, "tol_ratio": 1.5,
+            "ok": bool(ratio.max() <= 1.5 and ratio.min() >= 1.0 / 1.5),
             "fp32_operator": "matrix-free Siddon, FP32 (K11 xct_siddon_project_f32)"}
     out["seconds"] = time.perf_counter() - t0
     out["ok"] = all(v.get("ok", True) for v in out.values() if isinstance(v, dict))
@@ -364,7 +369,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--no-checks", action="store_true")
-    ap.add_argument("--check-iters", type=int, default=10)
+    ap.add_argument("--check-iters", type=int, default=30)
     ap.add_argument("--precision", default=None)
     ap.add_argument("--order", default="native")
     ap.add_argument("--no-e2e", action="store_true")
