@@ -143,6 +143,69 @@ int xct_format_export(const xct_format* f,
                       void* h_values /* [n_padded*row_group] of value_bytes */);
 void xct_format_free(xct_format* f);
 
+/* K5 on the device (row_group 1; staging keys that are a function of the
+ * column: image bands of A, view angles of A^T -- matrixstore.forward_plan
+ * / adjoint_plan).  Produces the same arrays as xct_format_build +
+ * upload (same footprints, groups, bank schedule and slab bytes), written
+ * straight into device memory.  Three passes per part of the operator
+ * (a chunk of views / a band of voxels):
+ *   ranges: lo/hi coordinate per (tile, key) [n_cta * n_keys], footprint
+ *           span per tile (bits of the tile's touched-cell bitmap);
+ *   count:  per tile {n_groups, n_slots, max_group_slots, n_padded}
+ *           [n_cta * 4] and slab widths [n_cta * 256 * warps];
+ *   fill:   group maps, group_map_ptr[g+1], slab offsets/widths and the
+ *           slabs (packed slot<<20|fp16 words for half/mixed, slot<<4 +
+ *           f32/f64 values otherwise; slab arrays zeroed by the caller),
+ *           from per-tile bases {group, slot, entry} [n_cta * 3].
+ * d_flag (zeroed by the caller) collects reasons to fall back to the host
+ * builder: 1 row not key-sorted, 2 key above capacity, 4 > 256 groups per
+ * tile, 8 footprint above bm_words*32 bits, 16 schedule beyond its limits. */
+typedef struct {
+  const int64_t* d_indptr;     /* [n_rows+1], entry 0 of the part at 0     */
+  const int32_t* d_indices;    /* global column ids                        */
+  const double* d_values;
+  int64_t n_rows;
+  const int32_t* d_cta_rows;   /* [n_cta*rows_per_cta] part-local rows, -1 */
+  const int32_t* d_cta_mode;   /* [n_cta] 0: key=col/B, coord=col%B;
+                                  1: key=col%B, coord=col/B;
+                                  2: key=B-1-col%B, coord=col/B            */
+  int64_t n_cta, rows_per_cta, rows_per_warp;
+  int32_t base_b, n_keys, capacity;
+  int32_t sched_rq;            /* rows per quarter-warp of the bank model
+                                  (8 >> log2 lanes per row); <= 1: no
+                                  schedule, (key, CSR position) order      */
+} xct_fmtd_part;
+
+int64_t xct_fmtd_scratch_bytes(void);
+int xct_fmtd_ranges(const xct_fmtd_part* part, int32_t* d_lo, int32_t* d_hi, int64_t* d_span,
+                    int32_t* d_flag, void* stream);
+int xct_fmtd_count(const xct_fmtd_part* part, const int32_t* d_lo, const int32_t* d_hi,
+                   int32_t bm_words, int64_t* d_counts, int32_t* d_widths, int32_t* d_flag,
+                   void* stream);
+int xct_fmtd_fill(const xct_fmtd_part* part, const int32_t* d_lo, const int32_t* d_hi,
+                  int32_t bm_words, const int32_t* d_widths, const int64_t* d_tile_base,
+                  int precision, int value_scale_exp, int32_t* d_group_map,
+                  int64_t* d_group_map_ptr, int64_t* d_slab_off, int32_t* d_slab_width,
+                  uint16_t* d_slots, void* d_values, void* d_scratch, int64_t scratch_bytes,
+                  int32_t* d_flag, uint64_t* d_qstats, void* stream);
+
+/* K4 on the device: entries per column in [col_lo, col_hi) of a device CSR
+ * (atomic adds into d_counts, zeroed by the caller) and the band transpose:
+ * rows [0, n_rows) of the CSR (global row id row_base + r), in passes of
+ * rows_per_pass rows, scattered into the rows of A^T for columns
+ * [col_lo, col_hi) at d_t_indptr[v] + cursor[v] and each pass's segment
+ * of every row sorted by row id -- so calling it for consecutive CSR chunks
+ * in ascending row order yields rows in ascending row id, exactly
+ * xct_csr_transpose / src/matrixstore.py:189-201 (d_cursor, d_prev zeroed
+ * per band by the caller). */
+int xct_csr_col_counts(const int64_t* d_indptr, const int32_t* d_indices, int64_t n_rows,
+                       int32_t col_lo, int32_t col_hi, int64_t* d_counts, void* stream);
+int xct_csr_transpose_band(const int64_t* d_indptr, const int32_t* d_indices,
+                           const double* d_values, int64_t n_rows, int64_t row_base,
+                           int64_t rows_per_pass, int32_t col_lo, int32_t col_hi,
+                           const int64_t* d_t_indptr, int32_t* d_cursor, int32_t* d_prev,
+                           int32_t* d_t_rows, double* d_t_vals, void* stream);
+
 /* stable counting transpose of a CSR block (src/matrixstore.py:189-201);
  * h_t_indptr [n_cols+1], h_t_indices/h_t_values [nnz]. */
 int xct_csr_transpose(int64_t n_rows, int64_t n_cols, const int64_t* h_indptr,

@@ -39,6 +39,13 @@ class Staged(C.Structure):
                 ("contract", i32), ("chunk_group", i32), ("row_group", i32)]
 
 
+class FmtdPart(C.Structure):
+    _fields_ = [("d_indptr", vp), ("d_indices", vp), ("d_values", vp), ("n_rows", i64),
+                ("d_cta_rows", vp), ("d_cta_mode", vp), ("n_cta", i64), ("rows_per_cta", i64),
+                ("rows_per_warp", i64), ("base_b", i32), ("n_keys", i32), ("capacity", i32),
+                ("sched_rq", i32)]
+
+
 class Epilogue(C.Structure):
     _fields_ = [("d_out", vp), ("row_stride", i64), ("chunk_stride", i64),
                 ("valid_cols", i32), ("ffactor", i32), ("value_scale_exp", i32),
@@ -58,6 +65,14 @@ _SIGS = {
     "xct_format_get_info": (i32, [vp, C.POINTER(FormatInfo)]),
     "xct_format_export": (i32, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "xct_format_free": (None, [vp]),
+    "xct_fmtd_scratch_bytes": (i64, []),
+    "xct_fmtd_ranges": (i32, [C.POINTER(FmtdPart), vp, vp, vp, vp, vp]),
+    "xct_fmtd_count": (i32, [C.POINTER(FmtdPart), vp, vp, i32, vp, vp, vp, vp]),
+    "xct_fmtd_fill": (i32, [C.POINTER(FmtdPart), vp, vp, i32, vp, vp, i32, i32, vp, vp, vp, vp,
+                            vp, vp, vp, i64, vp, vp, vp]),
+    "xct_csr_col_counts": (i32, [vp, vp, i64, i32, i32, vp, vp]),
+    "xct_csr_transpose_band": (i32, [vp, vp, vp, i64, i64, i64, i32, i32, vp, vp, vp, vp, vp,
+                                     vp]),
     "xct_csr_transpose": (i32, [i64, i64, vp, vp, vp, vp, vp, vp, i32]),
     "xct_spmm": (i32, [C.POINTER(Staged), i32, vp, i64, i64, i32, C.POINTER(Epilogue), i64, vp]),
     "xct_csr_spmm_f64": (i32, [vp, vp, vp, i64, vp, i64, vp, vp]),
@@ -130,7 +145,8 @@ KERNELS_PER_CALL = {"xct_dot": 2, "xct_sum_f64": 1, "xct_spmm": 1, "xct_maxabs":
                     "xct_csr_filter_cols": 1, "xct_csr_filter_map": 1, "xct_gather_rows": 1,
                     "xct_accumulate_rows": 1, "xct_scale_chunks": 2,
                     "xct_rows_to_chunked": 2, "xct_unchunk_rows_f64": 1,
-                    "xct_siddon_project_f32": 1}
+                    "xct_siddon_project_f32": 1, "xct_fmtd_ranges": 1, "xct_fmtd_count": 1,
+                    "xct_fmtd_fill": 1, "xct_csr_col_counts": 1}
 launch_count = [0]
 
 

@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -620,6 +621,207 @@ def upload_format(hf, precision: str, ffactor: int, n_in: int, n_out: int,
     T["group_map_ptr"][tot["n_groups"]] = s_off
     side = DeviceSide(precision, ffactor, f_dev, n_in, n_out, value_scale_exp, info, T,
                       plan_kind=parts[0].plan_kind)
+    return attach(side)
+
+
+# ---------------------------------------------------------------------------
+# K5 on the device (csrc/format_device.cu): same arrays as build_format +
+# upload_format for the band / view-key plans with one row per lane set
+# ---------------------------------------------------------------------------
+
+PAD_ENTRIES = 1024      # the kernel's load ring reads up to 4 steps past a slab
+_FMTD_SCRATCH = {}
+
+
+class DeviceBuildUnsupported(Exception):
+    """The device builder declined (limits or row order): use the host one."""
+
+
+def device_build_supported(plan: Plan, precision: str) -> bool:
+    return plan.kind in ("forward", "adjoint") and int(plan.row_group) == 1 and \
+        os.environ.get("XCT_HOST_BUILD") != "1"
+
+
+def _sched_rq(plan: Plan, precision: str, ffactor: int, schedule: bool) -> int:
+    """Rows per quarter-warp of the bank model (format_build.cpp BankModel)."""
+    if not schedule:
+        return 0
+    lg = (32 // plan.rows_per_warp).bit_length() - 1
+    return (8 >> lg) if lg <= 3 else 1
+
+
+@dataclass
+class DevicePart:
+    """One part (a chunk of views / a band of voxels) of a device-built side."""
+
+    tensors: dict
+    info: dict
+    cta_rows: np.ndarray
+    plan_kind: str
+
+
+def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int, plan: Plan,
+                        precision: str, ffactor: int, value_scale_exp: int, smem_budget: int,
+                        schedule: bool, base_b: int, n_keys: int, dev, pad: bool = True
+                        ) -> DevicePart:
+    """Device K5 of one part: ``d_*`` is the part's device CSR (row ids as in
+    ``plan.cta_rows``, global column ids); ``base_b``/``n_keys`` define the
+    key/coordinate of a column (grid_n, grid_n for A; detectors, views for
+    A^T).  Raises DeviceBuildUnsupported when the host builder must do it."""
+    import torch
+    if not device_build_supported(plan, precision):
+        raise DeviceBuildUnsupported("plan kind or row group")
+    f_dev = f_dev_for(ffactor, precision)
+    rec = f_dev * element_bytes(precision)
+    capacity = min(65536 // 16, max(1, smem_budget // (2 * rec)))
+    L = _lib.lib()
+    st = _lib.stream_handle(dev)
+    rows = np.ascontiguousarray(plan.cta_rows, np.int32)
+    n_cta, rpc = rows.shape
+    rpw = int(plan.rows_per_warp)
+    warps = rpc // rpw
+    d_rows = torch.from_numpy(rows.reshape(-1)).to(dev)
+    modes = np.ascontiguousarray(plan.cta_table, np.int32) if plan.kind == "forward" \
+        else np.zeros(n_cta, np.int32)
+    d_modes = torch.from_numpy(modes).to(dev)
+    part = _lib.FmtdPart(d_indptr.data_ptr(), d_indices.data_ptr(), d_values.data_ptr(),
+                         int(n_rows), d_rows.data_ptr(), d_modes.data_ptr(), int(n_cta), int(rpc),
+                         rpw, int(base_b), int(n_keys), int(capacity),
+                         _sched_rq(plan, precision, ffactor, schedule))
+    i32, i64 = torch.int32, torch.int64
+    flag = torch.zeros(1, dtype=i32, device=dev)
+    lo = torch.empty(max(n_cta * n_keys, 1), dtype=i32, device=dev)
+    hi = torch.empty_like(lo)
+    span = torch.zeros(max(n_cta, 1), dtype=i64, device=dev)
+    _lib.check(L.xct_fmtd_ranges(C.byref(part), lo.data_ptr(), hi.data_ptr(), span.data_ptr(),
+                                 flag.data_ptr(), st), "xct_fmtd_ranges")
+    bm_words = int(span.max().item()) // 32 + 2 if n_cta else 1
+    counts = torch.zeros((max(n_cta, 1), 4), dtype=i64, device=dev)
+    widths = torch.zeros(max(n_cta, 1) * 256 * warps, dtype=i32, device=dev)
+    stc = L.xct_fmtd_count(C.byref(part), lo.data_ptr(), hi.data_ptr(), bm_words,
+                           counts.data_ptr(), widths.data_ptr(), flag.data_ptr(), st)
+    if stc == _lib.XCT_ESTAGE:
+        raise DeviceBuildUnsupported("tile footprint exceeds shared memory")
+    _lib.check(stc, "xct_fmtd_count")
+    fl = int(flag.item())
+    if fl:
+        raise DeviceBuildUnsupported(f"count flags {fl}")
+    cnt = counts.cpu().numpy()[:n_cta]
+    ng, ns, mgs, npad = (cnt[:, i] for i in range(4))
+    base = np.zeros((max(n_cta, 1), 3), np.int64)
+    base[1:n_cta, 0] = np.cumsum(ng)[:-1]
+    base[1:n_cta, 1] = np.cumsum(ns)[:-1]
+    base[1:n_cta, 2] = np.cumsum(npad)[:-1]
+    n_groups, n_slots, n_padded = int(ng.sum()), int(ns.sum()), int(npad.sum())
+    T = {}
+    T["cta_group_ptr"] = torch.from_numpy(
+        np.concatenate(([0], np.cumsum(ng))).astype(np.int32)).to(dev)
+    T["group_map_ptr"] = torch.zeros(n_groups + 1, dtype=i64, device=dev)
+    T["group_map"] = torch.zeros(max(n_slots, 1), dtype=i32, device=dev)
+    T["slab_off"] = torch.zeros(max(n_groups * warps, 1), dtype=i64, device=dev)
+    T["slab_width"] = torch.zeros(max(n_groups * warps, 1), dtype=i32, device=dev)
+    T["cta_rows"] = d_rows
+    extra = PAD_ENTRIES if pad else 0
+    packed = precision in ("half", "mixed")
+    if packed:
+        T["values"] = torch.zeros(n_padded + extra, dtype=i32, device=dev)
+        T["slots"] = torch.zeros(1, dtype=torch.int16, device=dev)
+    else:
+        T["values"] = torch.zeros(n_padded + extra, dtype=torch.float64 if precision == "double"
+                                  else torch.float32, device=dev)
+        T["slots"] = torch.zeros(n_padded + extra, dtype=torch.int16, device=dev)
+    key = str(dev)
+    scratch = _FMTD_SCRATCH.get(key)
+    if scratch is None:
+        scratch = _FMTD_SCRATCH[key] = torch.empty(int(L.xct_fmtd_scratch_bytes()),
+                                                   dtype=torch.uint8, device=dev)
+    qs = torch.zeros(2, dtype=i64, device=dev)
+    d_base = torch.from_numpy(base).to(dev)
+    _lib.check(L.xct_fmtd_fill(C.byref(part), lo.data_ptr(), hi.data_ptr(), bm_words,
+                               widths.data_ptr(), d_base.data_ptr(), _lib.PREC_CODE[precision],
+                               int(value_scale_exp), T["group_map"].data_ptr(),
+                               T["group_map_ptr"].data_ptr(), T["slab_off"].data_ptr(),
+                               T["slab_width"].data_ptr(),
+                               None if packed else T["slots"].data_ptr(), T["values"].data_ptr(),
+                               scratch.data_ptr(), scratch.numel(), flag.data_ptr(), qs.data_ptr(),
+                               st), "xct_fmtd_fill")
+    fl = int(flag.item())
+    if fl:
+        raise DeviceBuildUnsupported(f"fill flags {fl}")
+    q = qs.cpu().numpy()
+    nnz = int((d_indptr[n_rows] - d_indptr[0]).item())
+    info = dict(n_cta=int(n_cta), rows_per_cta=int(rpc), rows_per_warp=rpw,
+                warps_per_cta=int(warps), n_groups=n_groups, n_slots=n_slots, n_padded=n_padded,
+                nnz=nnz, max_group_slots=int(mgs.max()) if n_cta else 0,
+                value_bytes=element_bytes(precision),
+                max_rel_quant_error=float(q[:1].view(np.float64)[0]),
+                underflow_count=int(q[1]), row_group=1)
+    return DevicePart(T, info, rows.reshape(-1), plan.kind)
+
+
+def combine_device_parts(parts: list, precision: str, ffactor: int, n_in: int, n_out: int,
+                         value_scale_exp: int, dev) -> "DeviceSide":
+    """Concatenate device-built parts over disjoint CTA tiles (offsets
+    rebased, as upload_format does for host parts); each part's tensors are
+    released as soon as they are copied."""
+    import torch
+    f_dev = f_dev_for(ffactor, precision)
+    if len(parts) == 1:
+        P = parts[0]
+        T = P.tensors
+        parts.clear()
+    else:
+        tot = {k: sum(int(p.info[k]) for p in parts)
+               for k in ("n_cta", "n_groups", "n_slots", "n_padded")}
+        warps = int(parts[0].info["warps_per_cta"])
+        rpc = int(parts[0].info["rows_per_cta"])
+        packed = precision in ("half", "mixed")
+        T = {"cta_group_ptr": torch.empty(tot["n_cta"] + 1, dtype=torch.int32, device=dev),
+             "group_map_ptr": torch.empty(tot["n_groups"] + 1, dtype=torch.int64, device=dev),
+             "group_map": torch.empty(max(tot["n_slots"], 1), dtype=torch.int32, device=dev),
+             "slab_off": torch.empty(max(tot["n_groups"] * warps, 1), dtype=torch.int64,
+                                     device=dev),
+             "slab_width": torch.empty(max(tot["n_groups"] * warps, 1), dtype=torch.int32,
+                                       device=dev),
+             "cta_rows": torch.empty(tot["n_cta"] * rpc, dtype=torch.int32, device=dev)}
+        vt = parts[0].tensors["values"].dtype
+        T["values"] = torch.zeros(tot["n_padded"] + PAD_ENTRIES, dtype=vt, device=dev)
+        T["slots"] = (torch.zeros(1, dtype=torch.int16, device=dev) if packed else
+                      torch.zeros(tot["n_padded"] + PAD_ENTRIES, dtype=torch.int16, device=dev))
+        c_off = g_off = s_off = e_off = 0
+        infos = [p.info for p in parts]
+        for P in parts:
+            A, inf = P.tensors, P.info
+            nc, ng = int(inf["n_cta"]), int(inf["n_groups"])
+            ns, ne = int(inf["n_slots"]), int(inf["n_padded"])
+            T["cta_group_ptr"][c_off:c_off + nc] = A["cta_group_ptr"][:nc] + g_off
+            T["group_map_ptr"][g_off:g_off + ng] = A["group_map_ptr"][:ng] + s_off
+            T["group_map"][s_off:s_off + ns] = A["group_map"][:ns]
+            T["slab_off"][g_off * warps:(g_off + ng) * warps] = A["slab_off"][:ng * warps] + e_off
+            T["slab_width"][g_off * warps:(g_off + ng) * warps] = A["slab_width"][:ng * warps]
+            T["cta_rows"][c_off * rpc:(c_off + nc) * rpc] = A["cta_rows"][:nc * rpc]
+            T["values"][e_off:e_off + ne] = A["values"][:ne]
+            if not packed:
+                T["slots"][e_off:e_off + ne] = A["slots"][:ne]
+            P.tensors = None               # release this part's device arrays
+            c_off, g_off, s_off, e_off = c_off + nc, g_off + ng, s_off + ns, e_off + ne
+        T["cta_group_ptr"][c_off] = g_off
+        T["group_map_ptr"][g_off] = s_off
+        P = parts[0]
+        P.info = dict(infos[0])
+        for k in ("n_cta", "n_groups", "n_slots", "n_padded", "nnz", "underflow_count"):
+            P.info[k] = sum(int(i[k]) for i in infos)
+        P.info["max_group_slots"] = max(int(i["max_group_slots"]) for i in infos)
+        P.info["max_rel_quant_error"] = max(float(i["max_rel_quant_error"]) for i in infos)
+        parts.clear()
+    info = _lib.FormatInfo()
+    for f, v in P.info.items():
+        setattr(info, f, v)
+    plane_slots = -(-int(info.max_group_slots) // 8) * 8
+    if plane_slots * 16 > 65536:
+        raise StageSplitRequired("load group too large for 16-bit plane offsets")
+    side = DeviceSide(precision, ffactor, f_dev, n_in, n_out, value_scale_exp, info, T,
+                      plan_kind=P.plan_kind)
     return attach(side)
 
 

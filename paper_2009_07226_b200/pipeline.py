@@ -231,6 +231,34 @@ def row_block_transposed(ip, ix, v, rows):
     return t_ip, t_ix, t_v, fp
 
 
+def key_shape(geometry, kind):
+    """(base B, number of keys) of the device builder's column -> (key,
+    coordinate) map: image bands of A (grid_n, grid_n), views of A^T
+    (detectors, views)."""
+    if kind == "forward":
+        return geometry.grid_n, geometry.grid_n
+    return geometry.num_detector_cols, geometry.num_angles
+
+
+def device_side_from_csr(geometry, cfg, plan, ip, ix, v, n_rows, n_cols, exp, budget, dev):
+    """K5 on the device from a host CSR (uploaded); None if the device
+    builder declines (the caller falls back to the host builder)."""
+    import torch
+    b, nk = key_shape(geometry, plan.kind)
+    d_ip = torch.from_numpy(np.ascontiguousarray(ip, np.int64)).to(dev)
+    d_ix = torch.from_numpy(np.ascontiguousarray(ix, np.int32)).to(dev)
+    d_v = torch.from_numpy(np.ascontiguousarray(v, np.float64)).to(dev)
+    try:
+        part = matrixstore.build_format_device(d_ip, d_ix, d_v, n_rows, n_cols, plan,
+                                               cfg.precision, cfg.ffactor, exp, budget,
+                                               cfg.order == "native", b, nk, dev)
+    except matrixstore.DeviceBuildUnsupported as e:
+        _log(f"device format build declined ({e}); host builder")
+        return None
+    return matrixstore.combine_device_parts([part], cfg.precision, cfg.ffactor, n_cols, n_rows,
+                                            exp, dev)
+
+
 class AssembledSystem:
     """Distributed forward/adjoint operator over one batch group's slices
     (src/pipeline.py:64-210), device resident."""
@@ -301,10 +329,15 @@ class AssembledSystem:
     def _single_side(self, ip, ix, v, n_rows, n_cols, kind) -> _Side:
         cfg = self.config
         plan = self._plan(ip, ix, n_rows, n_cols, kind)
-        blk = matrixstore.build_device_side(ip, ix, v, n_rows, n_cols, plan, cfg.precision,
-                                            cfg.ffactor, self.value_scale_exp,
-                                            self._budget(plan), self.device,
-                                            schedule=cfg.order == "native")
+        blk = None
+        if matrixstore.device_build_supported(plan, cfg.precision):
+            blk = device_side_from_csr(self.geometry, cfg, plan, ip, ix, v, n_rows, n_cols,
+                                       self.value_scale_exp, self._budget(plan), self.device)
+        if blk is None:
+            blk = matrixstore.build_device_side(ip, ix, v, n_rows, n_cols, plan, cfg.precision,
+                                                cfg.ffactor, self.value_scale_exp,
+                                                self._budget(plan), self.device,
+                                                schedule=cfg.order == "native")
         ident = np.arange(n_rows)
         return _Side([blk], [None], [None], [ident], n_cols, n_rows)
 
@@ -521,6 +554,13 @@ class _Timer:
         self.t = now
 
 
+def Plan_probe(cfg):
+    """A plan-shaped probe of what the streamed build would run (plan kind
+    and row group) for device_build_supported."""
+    return matrixstore.Plan(np.zeros((0, 1), np.int32), np.zeros((1, 1), np.int32),
+                            np.zeros(0, np.int32), 1, "forward", cfg.row_group_effective)
+
+
 class StreamedAssembly:
     """Operator build that never holds the whole matrix (needed at 2048^2 x
     2048 views, 1.03e10 entries): Siddon is regenerated on the device per
@@ -696,6 +736,111 @@ class StreamedAssembly:
         _log(f"adjoint build {tm.acc}")
         return side
 
+    # --- K4/K5 on the device ------------------------------------------------
+    BAND_NNZ_DEV = 2.5e9     # entries of one device A^T band (12 B each)
+
+    def _device_ok(self) -> bool:
+        cfg = self.cfg
+        probe = Plan_probe(cfg)
+        return matrixstore.device_build_supported(probe, cfg.precision)
+
+    def _forward_device(self, exp, col_counts):
+        """Projection format on the device, chunk of views by chunk; also
+        counts each voxel's entries (the back projection's row lengths)."""
+        import torch
+        cfg, g = self.cfg, self.g
+        n = g.grid_n
+        ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta, 1)
+        st = _lib.stream_handle(self.dev)
+        parts = []
+        tm = _Timer()
+        for k0, k1 in self._chunks(ta):
+            plan = matrixstore.forward_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, k0, k1,
+                                            row_group=1)
+            plan = matrixstore.assign_forward_regimes(plan, g.angles, n)
+            base = k0 * n
+            plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - base, -1).astype(np.int32)
+            tm.lap("plan")
+            ip, ix, v = self._siddon(k0, k1)
+            rows = (k1 - k0) * n
+            _lib.call("xct_csr_col_counts", ip.data_ptr(), ix.data_ptr(), rows, 0, g.num_voxels,
+                      col_counts.data_ptr(), st)
+            tm.lap("siddon")
+            part = matrixstore.build_format_device(ip, ix, v, rows, g.num_voxels, plan,
+                                                   cfg.precision, cfg.ffactor, exp,
+                                                   cfg.smem_budget_effective,
+                                                   cfg.order == "native", n, n, self.dev)
+            cr = part.tensors["cta_rows"]
+            part.tensors["cta_rows"] = torch.where(cr >= 0, cr + base, cr)
+            parts.append(part)
+            self.nnz += int(part.info["nnz"])
+            del ip, ix, v
+            tm.lap("format")
+        side = matrixstore.combine_device_parts(parts, cfg.precision, cfg.ffactor, g.num_voxels,
+                                                g.num_rays, exp, self.dev)
+        torch.cuda.synchronize(self.dev)
+        tm.lap("combine")
+        _log(f"forward build (device) {tm.acc}")
+        return side
+
+    def _adjoint_device(self, exp, chunks, col_counts):
+        """Back projection format on the device, band of voxel rows by band:
+        the band's A^T rows (ascending ray id) by the device transpose, then
+        device K5."""
+        import torch
+        cfg, g = self.cfg, self.g
+        n, R = g.grid_n, g.num_rays
+        tz = matrixstore.adjoint_tile_height(n, self.rw, cfg.warps_per_cta, 1)
+        st = _lib.stream_handle(self.dev)
+        per_row = col_counts.view(n, n).sum(1).cpu().numpy()      # entries per image row
+        bands, z0 = [], 0
+        while z0 < n:
+            z1, acc = z0, 0
+            while z1 < n and (z1 == z0 or acc + per_row[z1:z1 + tz].sum() <= self.BAND_NNZ_DEV):
+                acc += per_row[z1:z1 + tz].sum()
+                z1 = min(n, z1 + tz)
+            bands.append((z0, z1))
+            z0 = z1
+        parts = []
+        tm = _Timer()
+        for z0, z1 in bands:
+            lo, hi = z0 * n, z1 * n
+            nb = hi - lo
+            t_ip = torch.zeros(nb + 1, dtype=torch.int64, device=self.dev)
+            torch.cumsum(col_counts[lo:hi], 0, out=t_ip[1:])
+            m = int(t_ip[-1].item())
+            t_rows = torch.empty(max(m, 1), dtype=torch.int32, device=self.dev)
+            t_vals = torch.empty(max(m, 1), dtype=torch.float64, device=self.dev)
+            cursor = torch.zeros(nb, dtype=torch.int32, device=self.dev)
+            prev = torch.zeros(nb, dtype=torch.int32, device=self.dev)
+            for k0, k1 in chunks:
+                ip, ix, v = self._siddon(k0, k1)
+                _lib.call("xct_csr_transpose_band", ip.data_ptr(), ix.data_ptr(), v.data_ptr(),
+                          (k1 - k0) * n, k0 * n, 32 * n, lo, hi, t_ip.data_ptr(),
+                          cursor.data_ptr(), prev.data_ptr(), t_rows.data_ptr(),
+                          t_vals.data_ptr(), st)
+                del ip, ix, v
+            tm.lap("siddon+transpose")
+            plan = matrixstore.adjoint_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, z0, z1,
+                                            row_group=1)
+            plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - lo, -1).astype(np.int32)
+            part = matrixstore.build_format_device(t_ip, t_rows, t_vals, nb, R, plan,
+                                                   cfg.precision, cfg.ffactor, exp,
+                                                   cfg.smem_budget_effective,
+                                                   cfg.order == "native",
+                                                   g.num_detector_cols, g.num_angles, self.dev)
+            cr = part.tensors["cta_rows"]
+            part.tensors["cta_rows"] = torch.where(cr >= 0, cr + lo, cr)
+            parts.append(part)
+            del t_ip, t_rows, t_vals, cursor, prev
+            tm.lap("format")
+        side = matrixstore.combine_device_parts(parts, cfg.precision, cfg.ffactor, R,
+                                                g.num_voxels, exp, self.dev)
+        torch.cuda.synchronize(self.dev)
+        tm.lap("combine")
+        _log(f"adjoint build (device) {tm.acc}")
+        return side
+
     def run(self) -> AssembledSystem:
         import torch
         from .parallel import MatrixInfo
@@ -704,6 +849,18 @@ class StreamedAssembly:
         chunks = self._chunks(ta)
         exp = self._exponent(chunks) if cfg.precision in ("half", "mixed") else 0
         self.nnz = 0
+        if self._device_ok():
+            try:
+                counts = torch.zeros(g.num_voxels, dtype=torch.int64, device=self.dev)
+                fwd = self._forward_device(exp, counts)
+                adj = self._adjoint_device(exp, chunks, counts)
+                info = MatrixInfo(g.num_rays, g.num_voxels, self.nnz, g.num_angles,
+                                  g.num_detector_cols)
+                return AssembledSystem.from_sides(info, cfg, g, fwd, adj, exp)
+            except matrixstore.DeviceBuildUnsupported as e:
+                _log(f"device format build declined ({e}); host builder")
+                self.nnz = 0
+                torch.cuda.empty_cache()
         fwd = self._forward(exp)
         self._pool.clear()
         import gc

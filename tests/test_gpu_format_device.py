@@ -1,0 +1,130 @@
+"""The device format builder (K4/K5 on the GPU, csrc/format_device.cu)
+against the host builder (format_build.cpp), byte for byte: same load
+groups, same group maps, same bank schedule, same slab words -- and the
+streamed device build of a whole operator against the monolithic host
+build (replaces src/matrixstore.py:189-201, :250-262, :417-562)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2009_07226_b200 import _lib, geometry, matrixstore, pipeline
+
+pytestmark = pytest.mark.gpu
+
+
+def _host_words(hf, precision):
+    """The host format's slab entries encoded as upload_format stores them."""
+    slots = hf.arrays["slots"].astype(np.int64) & 0xFFFF
+    off = slots << 4
+    if precision in ("half", "mixed"):
+        bits = hf.arrays["values"].view(np.uint16).astype(np.int64)
+        return ((off << 16) | bits).astype(np.uint32).view(np.int32), None
+    return hf.arrays["values"], off.astype(np.uint16).view(np.int16)
+
+
+def _compare(hf, part, precision):
+    for k in ("n_cta", "n_groups", "n_slots", "n_padded", "nnz", "max_group_slots",
+              "underflow_count"):
+        assert int(hf.info[k]) == int(part.info[k]), k
+    assert float(hf.info["max_rel_quant_error"]) == pytest.approx(
+        float(part.info["max_rel_quant_error"]), rel=0, abs=0)
+    T = {k: v.cpu().numpy() for k, v in part.tensors.items()}
+    for k in ("cta_group_ptr", "group_map_ptr", "group_map", "slab_off", "slab_width"):
+        n = len(hf.arrays[k])
+        assert np.array_equal(T[k][:n], hf.arrays[k]), k
+    vals, slots = _host_words(hf, precision)
+    n = int(hf.info["n_padded"])
+    assert np.array_equal(T["values"][:n], vals), "slab values"
+    assert not T["values"][n:].any()
+    if slots is not None:
+        assert np.array_equal(T["slots"][:n], slots), "slab slots"
+
+
+CASES = [(96, 64, "mixed", True), (96, 64, "mixed", False), (180, 128, "mixed", True),
+         (64, 48, "single", True), (64, 48, "double", True), (48, 40, "half", True)]
+
+
+@pytest.mark.parametrize("k,n,precision,schedule", CASES)
+def test_device_builder_equals_host_builder(k, n, precision, schedule):
+    g = geometry.make_geometry(k, 1, n)
+    A = geometry.build_system_matrix(g)
+    ip, ix, v = A.host_csr32()
+    cfg = pipeline.SystemConfig(precision=precision, ffactor=16, row_group=1)
+    rw = pipeline._rows_per_warp(cfg)
+    dev = geometry.device()
+    exp = matrixstore.half_rescale_exponent(np.asarray(v)) if precision in ("half", "mixed") \
+        else 0
+    budget = cfg.smem_budget_effective
+    t_ip, t_ix, t_v = pipeline._transpose(ip, ix, v, g.num_rays, g.num_voxels)
+    sides = [("forward", ip, ix, v, g.num_rays, g.num_voxels,
+              matrixstore.assign_forward_regimes(
+                  matrixstore.forward_plan(k, n, rw, cfg.warps_per_cta), g.angles, n)),
+             ("adjoint", t_ip, t_ix, t_v, g.num_voxels, g.num_rays,
+              matrixstore.adjoint_plan(k, n, rw, cfg.warps_per_cta))]
+    for kind, a, b, c, nr, nc, plan in sides:
+        hf = matrixstore.build_format(a, b, c, nr, nc, plan, precision, 16, exp, budget,
+                                      schedule=schedule)
+        B, nk = pipeline.key_shape(g, kind)
+        part = matrixstore.build_format_device(
+            torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev),
+            torch.from_numpy(c).to(dev), nr, nc, plan, precision, 16, exp, budget, schedule,
+            B, nk, dev)
+        _compare(hf, part, precision)
+        print(f"{kind} k={k} n={n} {precision} schedule={schedule}: device format == host "
+              f"format ({hf.info['n_padded']} slab entries, {hf.info['n_groups']} groups)")
+
+
+def test_device_band_transpose_equals_host_transpose():
+    g = geometry.make_geometry(64, 1, 48)
+    A = geometry.build_system_matrix(g)
+    ip, ix, v = A.host_csr32()
+    t_ip, t_ix, t_v = pipeline._transpose(ip, ix, v, g.num_rays, g.num_voxels)
+    dev = geometry.device()
+    st = _lib.stream_handle(dev)
+    n = g.grid_n
+    for z0, z1 in ((0, 16), (16, 48)):
+        lo, hi = z0 * n, z1 * n
+        counts = torch.zeros(hi - lo, dtype=torch.int64, device=dev)
+        chunks = [(0, 20), (20, 45), (45, 64)]
+        csrs = [geometry.siddon_csr(g, k0, k1, dev) for k0, k1 in chunks]
+        for (k0, k1), (c_ip, c_ix, _) in zip(chunks, csrs):
+            _lib.call("xct_csr_col_counts", c_ip.data_ptr(), c_ix.data_ptr(), (k1 - k0) * n, lo,
+                      hi, counts.data_ptr(), st)
+        d_ip = torch.zeros(hi - lo + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(counts, 0, out=d_ip[1:])
+        m = int(d_ip[-1])
+        rows = torch.empty(m, dtype=torch.int32, device=dev)
+        vals = torch.empty(m, dtype=torch.float64, device=dev)
+        cur = torch.zeros(hi - lo, dtype=torch.int32, device=dev)
+        prev = torch.zeros(hi - lo, dtype=torch.int32, device=dev)
+        for (k0, k1), (c_ip, c_ix, c_v) in zip(chunks, csrs):
+            _lib.call("xct_csr_transpose_band", c_ip.data_ptr(), c_ix.data_ptr(), c_v.data_ptr(),
+                      (k1 - k0) * n, k0 * n, 7 * n, lo, hi, d_ip.data_ptr(), cur.data_ptr(),
+                      prev.data_ptr(), rows.data_ptr(), vals.data_ptr(), st)
+        want_ip = t_ip[lo:hi + 1] - t_ip[lo]
+        assert np.array_equal(d_ip.cpu().numpy(), want_ip)
+        assert np.array_equal(rows.cpu().numpy(), t_ix[t_ip[lo]:t_ip[hi]])
+        assert np.array_equal(vals.cpu().numpy(), t_v[t_ip[lo]:t_ip[hi]])
+
+
+@pytest.mark.parametrize("precision", ["mixed", "half"])
+def test_streamed_device_build_equals_monolithic_host_build(precision, monkeypatch):
+    """Whole operators: the streamed device build (chunks of views, bands of
+    voxels) gives the same projections, bit for bit, as the monolithic
+    host build."""
+    g = geometry.make_geometry(96, 16, 64)
+    monkeypatch.setenv("XCT_HOST_BUILD", "1")
+    host = pipeline.assemble(g, pipeline.SystemConfig(precision=precision, ffactor=16,
+                                                      build="monolithic"))
+    monkeypatch.delenv("XCT_HOST_BUILD")
+    monkeypatch.setattr(pipeline.StreamedAssembly, "CHUNK_NNZ", 2e5)    # several chunks
+    monkeypatch.setattr(pipeline.StreamedAssembly, "BAND_NNZ_DEV", 3e5)  # several bands
+    dev_sys = pipeline.assemble(g, pipeline.SystemConfig(precision=precision, ffactor=16,
+                                                         build="streamed"))
+    assert dev_sys.forward.blocks[0].hbm_bytes() > 0
+    rng = np.random.default_rng(4)
+    x = rng.random((g.num_voxels, 16)).astype(np.float32)
+    y = rng.random((g.num_rays, 16)).astype(np.float32)
+    assert np.array_equal(dev_sys.apply_forward(x)[0], host.apply_forward(x)[0])
+    assert np.array_equal(dev_sys.apply_adjoint(y)[0], host.apply_adjoint(y)[0])
