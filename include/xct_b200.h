@@ -174,6 +174,12 @@ typedef struct {
   int32_t sched_rq;            /* rows per quarter-warp of the bank model
                                   (8 >> log2 lanes per row); <= 1: no
                                   schedule, (key, CSR position) order      */
+  int32_t sched_fast;          /* 0: the host's schedule exactly (edge
+                                  colouring by alternating paths, one thread
+                                  per quarter -- slow at scale); 1: first-fit
+                                  over step masks for slabs <= 64 steps
+                                  (same entries per row and slab, other
+                                  step placement)                          */
 } xct_fmtd_part;
 
 int64_t xct_fmtd_scratch_bytes(void);

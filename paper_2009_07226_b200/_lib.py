@@ -43,7 +43,7 @@ class FmtdPart(C.Structure):
     _fields_ = [("d_indptr", vp), ("d_indices", vp), ("d_values", vp), ("n_rows", i64),
                 ("d_cta_rows", vp), ("d_cta_mode", vp), ("n_cta", i64), ("rows_per_cta", i64),
                 ("rows_per_warp", i64), ("base_b", i32), ("n_keys", i32), ("capacity", i32),
-                ("sched_rq", i32)]
+                ("sched_rq", i32), ("sched_fast", i32)]
 
 
 class Epilogue(C.Structure):

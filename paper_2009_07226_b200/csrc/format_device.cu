@@ -53,7 +53,7 @@ struct Part {
   const int32_t* cta_mode;
   int64_t n_cta;
   int32_t rows_per_cta, rows_per_warp, warps;
-  int32_t B, n_keys, capacity, rq;
+  int32_t B, n_keys, capacity, rq, fast;
 };
 
 __device__ __forceinline__ void key_coord(int mode, int32_t col, int B, int& key, int& coord) {
@@ -473,8 +473,170 @@ __device__ __forceinline__ void write_entry(const FillArgs& a, int64_t at, int s
   }
 }
 
+// Fast bank schedule of one (group, warp, quarter-warp): first fit over
+// step masks of NW 64-bit words (width <= 64 * NW) -- each entry takes the
+// first step where its row is free and no other row of the quarter reads
+// its bank class, else the first step where its row is free (one extra
+// wavefront).  Same entries per row and slab as the host schedule, other
+// steps: sums equal to rounding (native order).  Idle lanes re-read the
+// slot the quarter's first busy row reads at that step (broadcast), as the
+// host schedule does.
+template <int NW>
+__device__ void greedy_quarter(const FillArgs& a, const Tile& T, int64_t tile, int w, int q,
+                               int rq, int rpw, int width, int k0, int k1, int gsb, int64_t so,
+                               double scale, uint64_t* taken, double& wmax, int64_t& nunder) {
+  const Part& p = a.p;
+  const int cmask = rq - 1;
+  uint64_t valid[NW];
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    const int lo = k * 64;
+    valid[k] = width >= lo + 64 ? ~0ull : (width > lo ? ((1ull << (width - lo)) - 1ull) : 0ull);
+  }
+  for (int i = 0; i < 8 * NW; ++i) taken[i] = 0ull;
+  uint64_t used[kRqMax][NW];
+#pragma unroll
+  for (int rr = 0; rr < kRqMax; ++rr) {
+#pragma unroll
+    for (int k = 0; k < NW; ++k) used[rr][k] = 0ull;
+    if (rr >= rq) continue;
+    const int rin = q * rq + rr;
+    const int32_t r = p.cta_rows[tile * p.rows_per_cta + w * rpw + rin];
+    if (r < 0) continue;
+    const int64_t hi_j = p.indptr[r + 1];
+    int64_t L = p.indptr[r], H = hi_j;
+    while (L < H) {
+      const int64_t M = (L + H) >> 1;
+      int key, coord;
+      key_coord(T.mode, p.indices[M], p.B, key, coord);
+      if (key < k0) L = M + 1; else H = M;
+    }
+    for (int64_t j = L; j < hi_j; ++j) {
+      int key, coord;
+      key_coord(T.mode, p.indices[j], p.B, key, coord);
+      if (key >= k1) break;
+      const int slot = bit_rank(T, T.kbase[key] + coord - T.lo[key]) - gsb;
+      const int c = slot & cmask;
+      int n = -1;
+#pragma unroll
+      for (int k = 0; k < NW; ++k) {
+        const uint64_t m = ~used[rr][k] & ~taken[c * NW + k] & valid[k];
+        if (n < 0 && m) n = k * 64 + __ffsll((long long)m) - 1;
+      }
+      if (n < 0) {
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+          const uint64_t m = ~used[rr][k] & valid[k];
+          if (n < 0 && m) n = k * 64 + __ffsll((long long)m) - 1;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NW; ++k)
+        if ((n >> 6) == k) {
+          used[rr][k] |= 1ull << (n & 63);
+          taken[c * NW + k] |= 1ull << (n & 63);
+        }
+      write_entry(a, so + ((int64_t)(n >> 2) * rpw + rin) * 4 + (n & 3), slot, j, scale, wmax,
+                  nunder);
+    }
+  }
+  for (int n = 0; n < width; ++n) {
+    int src = -1;
+#pragma unroll
+    for (int rr = kRqMax - 1; rr >= 0; --rr) {
+      uint64_t bit = 0;
+#pragma unroll
+      for (int k = 0; k < NW; ++k)
+        if ((n >> 6) == k) bit = used[rr][k] >> (n & 63) & 1ull;
+      if (rr < rq && bit) src = rr;
+    }
+    if (src < 0) continue;
+    const int64_t at0 = so + ((int64_t)(n >> 2) * rpw + q * rq + src) * 4 + (n & 3);
+    const int slot = a.slots ? (a.slots[at0] >> 4) : (int)(((uint32_t*)a.values)[at0] >> 20);
+    if (slot <= 0) continue;
+#pragma unroll
+    for (int rr = 0; rr < kRqMax; ++rr) {
+      uint64_t bit = 1;
+#pragma unroll
+      for (int k = 0; k < NW; ++k)
+        if ((n >> 6) == k) bit = used[rr][k] >> (n & 63) & 1ull;
+      if (rr < rq && !bit)
+        write_entry(a, so + ((int64_t)(n >> 2) * rpw + q * rq + rr) * 4 + (n & 3), slot, -1,
+                    scale, wmax, nunder);
+    }
+  }
+}
+
+// greedy_quarter for slabs wider than 256 steps (tiles in the image corners
+// see a few rays per view, so one load group spans many views): the same
+// first fit with the step masks in the thread's global scratch, loops not
+// unrolled (keeps the common path's registers).
+constexpr int kWideWords = 16;
+__device__ __noinline__ void greedy_quarter_wide(const FillArgs& a, const Tile& T, int64_t tile,
+                                                 int w, int q, int rq, int rpw, int width, int k0,
+                                                 int k1, int gsb, int64_t so, double scale,
+                                                 uint64_t* used, uint64_t* taken, double& wmax,
+                                                 int64_t& nunder) {
+  const Part& p = a.p;
+  const int cmask = rq - 1;
+  const int nw = (width + 63) >> 6;
+  auto valid = [&](int k) {
+    const int lo = k * 64;
+    return width >= lo + 64 ? ~0ull : (width > lo ? ((1ull << (width - lo)) - 1ull) : 0ull);
+  };
+  for (int i = 0; i < kRqMax * kWideWords; ++i) used[i] = 0ull;
+  for (int i = 0; i < 8 * kWideWords; ++i) taken[i] = 0ull;
+  for (int rr = 0; rr < rq; ++rr) {
+    const int rin = q * rq + rr;
+    const int32_t r = p.cta_rows[tile * p.rows_per_cta + w * rpw + rin];
+    if (r < 0) continue;
+    const int64_t hi_j = p.indptr[r + 1];
+    int64_t L = p.indptr[r], H = hi_j;
+    while (L < H) {
+      const int64_t M = (L + H) >> 1;
+      int key, coord;
+      key_coord(T.mode, p.indices[M], p.B, key, coord);
+      if (key < k0) L = M + 1; else H = M;
+    }
+    for (int64_t j = L; j < hi_j; ++j) {
+      int key, coord;
+      key_coord(T.mode, p.indices[j], p.B, key, coord);
+      if (key >= k1) break;
+      const int slot = bit_rank(T, T.kbase[key] + coord - T.lo[key]) - gsb;
+      const int c = slot & cmask;
+      int n = -1;
+      for (int k = 0; k < nw && n < 0; ++k) {
+        const uint64_t m = ~used[rr * kWideWords + k] & ~taken[c * kWideWords + k] & valid(k);
+        if (m) n = k * 64 + __ffsll((long long)m) - 1;
+      }
+      for (int k = 0; k < nw && n < 0; ++k) {
+        const uint64_t m = ~used[rr * kWideWords + k] & valid(k);
+        if (m) n = k * 64 + __ffsll((long long)m) - 1;
+      }
+      used[rr * kWideWords + (n >> 6)] |= 1ull << (n & 63);
+      taken[c * kWideWords + (n >> 6)] |= 1ull << (n & 63);
+      write_entry(a, so + ((int64_t)(n >> 2) * rpw + rin) * 4 + (n & 3), slot, j, scale, wmax,
+                  nunder);
+    }
+  }
+  for (int n = 0; n < width; ++n) {
+    int src = -1;
+    for (int rr = 0; rr < rq && src < 0; ++rr)
+      if (used[rr * kWideWords + (n >> 6)] >> (n & 63) & 1ull) src = rr;
+    if (src < 0) continue;
+    const int64_t at0 = so + ((int64_t)(n >> 2) * rpw + q * rq + src) * 4 + (n & 3);
+    const int slot = a.slots ? (a.slots[at0] >> 4) : (int)(((uint32_t*)a.values)[at0] >> 20);
+    if (slot <= 0) continue;
+    for (int rr = 0; rr < rq; ++rr)
+      if (!(used[rr * kWideWords + (n >> 6)] >> (n & 63) & 1ull))
+        write_entry(a, so + ((int64_t)(n >> 2) * rpw + q * rq + rr) * 4 + (n & 3), slot, -1,
+                    scale, wmax, nunder);
+  }
+}
+
 __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
   extern __shared__ int32_t sm[];
+  __shared__ uint64_t s_taken[kFillThreads][8 * 4];
   const Part& p = a.p;
   Tile T;
   tile_carve(p, a.bm_words, sm, T);
@@ -532,6 +694,22 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
       int ja_of[kRqMax];
       int ne = 0;
       bool over = false;
+      if (sched && p.fast && width <= 64) {
+        greedy_quarter<1>(a, T, tile, w, q, rq, rpw, width, k0, k1, gsb, so, scale,
+                          s_taken[threadIdx.x], wmax, nunder);
+        continue;
+      }
+      if (sched && p.fast && width <= 256) {
+        greedy_quarter<4>(a, T, tile, w, q, rq, rpw, width, k0, k1, gsb, so, scale,
+                          s_taken[threadIdx.x], wmax, nunder);
+        continue;
+      }
+      if (sched && p.fast && width <= 64 * kWideWords) {   // image-corner tiles, rare
+        uint64_t* scr = reinterpret_cast<uint64_t*>(S.atL);       // this thread's scratch
+        greedy_quarter_wide(a, T, tile, w, q, rq, rpw, width, k0, k1, gsb, so, scale, scr,
+                            scr + kRqMax * kWideWords, wmax, nunder);
+        continue;
+      }
       // edges: rows of the quarter in order, each row's group span in order
       for (int rr = 0; rr < rq; ++rr) {
         const int rin = q * rq + rr;
@@ -667,6 +845,7 @@ int make_part(const xct_fmtd_part* in, Part& p) {
   p.n_keys = in->n_keys;
   p.capacity = in->capacity;
   p.rq = in->sched_rq;
+  p.fast = in->sched_fast;
   return XCT_OK;
 }
 

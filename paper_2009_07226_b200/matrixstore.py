@@ -255,22 +255,22 @@ def forward_tile_height(n: int, rows_per_warp: int, warps: int, row_group: int =
 
 
 def assign_forward_regimes(plan: Plan, angles, n: int) -> Plan:
-    """Pick the band key of every forward tile from its view angles."""
-    tabs = np.zeros(len(plan.cta_rows), np.int32)
+    """Pick the band key of every forward tile from its view angles: x
+    bands (ascending for cos > 0, descending for cos < 0) when every view of
+    the tile is shallow, z bands otherwise (z is non-decreasing along every
+    ray since sin >= 0)."""
     ang = np.asarray(angles, dtype=np.float64)
-    for b, rows in enumerate(plan.cta_rows):
-        rr = rows[rows >= 0]
-        if len(rr) == 0:
-            continue
-        th = ang[np.unique(rr // n)]
-        cs, sn = np.cos(th), np.sin(th)
-        if np.all(np.abs(cs) > np.abs(sn)) and np.all(cs > 0):
-            tabs[b] = 1
-        elif np.all(np.abs(cs) > np.abs(sn)) and np.all(cs < 0):
-            tabs[b] = 2
-        else:
-            tabs[b] = 0      # z is non-decreasing along every ray (sin >= 0)
-    plan.cta_table = tabs
+    cs, sn = np.cos(ang), np.sin(ang)
+    rows = plan.cta_rows
+    valid = rows >= 0
+    k = np.where(valid, rows // n, 0)
+    shallow = np.abs(cs) > np.abs(sn)
+    pos = shallow & (cs > 0)
+    neg = shallow & (cs < 0)
+    any_row = valid.any(axis=1)
+    all_pos = np.all(np.where(valid, pos[k], True), axis=1) & any_row
+    all_neg = np.all(np.where(valid, neg[k], True), axis=1) & any_row
+    plan.cta_table = np.where(all_pos, 1, np.where(all_neg, 2, 0)).astype(np.int32)
     return plan
 
 
@@ -662,12 +662,16 @@ class DevicePart:
 
 def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int, plan: Plan,
                         precision: str, ffactor: int, value_scale_exp: int, smem_budget: int,
-                        schedule: bool, base_b: int, n_keys: int, dev, pad: bool = True
-                        ) -> DevicePart:
+                        schedule: bool, base_b: int, n_keys: int, dev, pad: bool = True,
+                        exact: bool = False) -> DevicePart:
     """Device K5 of one part: ``d_*`` is the part's device CSR (row ids as in
     ``plan.cta_rows``, global column ids); ``base_b``/``n_keys`` define the
     key/coordinate of a column (grid_n, grid_n for A; detectors, views for
-    A^T).  Raises DeviceBuildUnsupported when the host builder must do it."""
+    A^T).  ``exact`` runs the host's bank schedule step for step (byte-
+    identical to build_format; one thread per quarter-warp, slow at scale);
+    the default first-fit schedule places the same entries in the same
+    slabs on other steps.  Raises DeviceBuildUnsupported when the host
+    builder must do it."""
     import torch
     if not device_build_supported(plan, precision):
         raise DeviceBuildUnsupported("plan kind or row group")
@@ -687,7 +691,8 @@ def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int,
     part = _lib.FmtdPart(d_indptr.data_ptr(), d_indices.data_ptr(), d_values.data_ptr(),
                          int(n_rows), d_rows.data_ptr(), d_modes.data_ptr(), int(n_cta), int(rpc),
                          rpw, int(base_b), int(n_keys), int(capacity),
-                         _sched_rq(plan, precision, ffactor, schedule))
+                         _sched_rq(plan, precision, ffactor, schedule),
+                         0 if exact or os.environ.get("XCT_FMTD_EXACT") == "1" else 1)
     i32, i64 = torch.int32, torch.int64
     flag = torch.zeros(1, dtype=i32, device=dev)
     lo = torch.empty(max(n_cta * n_keys, 1), dtype=i32, device=dev)
@@ -747,7 +752,7 @@ def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int,
                                st), "xct_fmtd_fill")
     fl = int(flag.item())
     if fl:
-        raise DeviceBuildUnsupported(f"fill flags {fl}")
+        raise DeviceBuildUnsupported(f"fill flags {fl}, widest slab {int(widths.max())} steps")
     q = qs.cpu().numpy()
     nnz = int((d_indptr[n_rows] - d_indptr[0]).item())
     info = dict(n_cta=int(n_cta), rows_per_cta=int(rpc), rows_per_warp=rpw,

@@ -69,10 +69,70 @@ def test_device_builder_equals_host_builder(k, n, precision, schedule):
         part = matrixstore.build_format_device(
             torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev),
             torch.from_numpy(c).to(dev), nr, nc, plan, precision, 16, exp, budget, schedule,
-            B, nk, dev)
+            B, nk, dev, exact=True)
         _compare(hf, part, precision)
         print(f"{kind} k={k} n={n} {precision} schedule={schedule}: device format == host "
               f"format ({hf.info['n_padded']} slab entries, {hf.info['n_groups']} groups)")
+
+
+def _row_entries(T_or_arrays, info, precision, host):
+    """Per (group, warp, row) the sorted nonzero slab entries (slot, value)."""
+    warps, rpw = int(info["warps_per_cta"]), int(info["rows_per_warp"])
+    if host:
+        vals, slots = _host_words(T_or_arrays, precision)
+        off, wid = T_or_arrays.arrays["slab_off"], T_or_arrays.arrays["slab_width"]
+    else:
+        T = {k: v.cpu().numpy() for k, v in T_or_arrays.tensors.items()}
+        vals, slots = T["values"], T["slots"] if precision not in ("half", "mixed") else None
+        off, wid = T["slab_off"], T["slab_width"]
+    out = []
+    for i in range(len(wid)):
+        W = int(wid[i])
+        if W == 0:
+            continue
+        blk = np.arange(W)[:, None] // 4 * rpw * 4 + np.arange(rpw)[None, :] * 4 + \
+            (np.arange(W) % 4)[:, None]
+        at = off[i] + blk                       # [step, row]
+        for r in range(rpw):
+            v = vals[at[:, r]]
+            if slots is None:
+                keep = (v.view(np.uint32) & 0xFFFF) != 0
+                out.append(np.sort(v[keep].view(np.uint32)))
+            else:
+                keep = v != 0
+                key = slots[at[:, r]][keep].astype(np.int64) * 2 ** 40 + \
+                    np.argsort(np.argsort(v[keep]))
+                out.append(np.sort(np.stack([slots[at[:, r]][keep].astype(np.float64),
+                                             v[keep].astype(np.float64)], 1), axis=0))
+    return out
+
+
+@pytest.mark.parametrize("k,n,precision", [(180, 128, "mixed"), (64, 48, "single")])
+def test_fast_schedule_places_the_same_entries(k, n, precision):
+    """The default first-fit schedule: identical groups, maps and slab
+    widths; every row holds the same entries in every slab, on other steps."""
+    g = geometry.make_geometry(k, 1, n)
+    A = geometry.build_system_matrix(g)
+    ip, ix, v = A.host_csr32()
+    cfg = pipeline.SystemConfig(precision=precision, ffactor=16, row_group=1)
+    rw = pipeline._rows_per_warp(cfg)
+    dev = geometry.device()
+    exp = matrixstore.half_rescale_exponent(np.asarray(v)) if precision == "mixed" else 0
+    plan = matrixstore.assign_forward_regimes(
+        matrixstore.forward_plan(k, n, rw, cfg.warps_per_cta), g.angles, n)
+    hf = matrixstore.build_format(ip, ix, v, g.num_rays, g.num_voxels, plan, precision, 16, exp,
+                                  cfg.smem_budget_effective, schedule=True)
+    part = matrixstore.build_format_device(
+        torch.from_numpy(ip).to(dev), torch.from_numpy(ix).to(dev), torch.from_numpy(v).to(dev),
+        g.num_rays, g.num_voxels, plan, precision, 16, exp, cfg.smem_budget_effective, True,
+        n, n, dev)
+    T = {k2: t.cpu().numpy() for k2, t in part.tensors.items()}
+    for k2 in ("cta_group_ptr", "group_map_ptr", "group_map", "slab_off", "slab_width"):
+        assert np.array_equal(T[k2][:len(hf.arrays[k2])], hf.arrays[k2]), k2
+    a = _row_entries(hf, hf.info, precision, True)
+    b = _row_entries(part, part.info, precision, False)
+    assert len(a) == len(b)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
 
 
 def test_device_band_transpose_equals_host_transpose():
@@ -111,9 +171,11 @@ def test_device_band_transpose_equals_host_transpose():
 @pytest.mark.parametrize("precision", ["mixed", "half"])
 def test_streamed_device_build_equals_monolithic_host_build(precision, monkeypatch):
     """Whole operators: the streamed device build (chunks of views, bands of
-    voxels) gives the same projections, bit for bit, as the monolithic
-    host build."""
+    voxels) with the host's exact schedule gives the same projections, bit
+    for bit, as the monolithic host build; with the default fast schedule
+    the same to rounding."""
     g = geometry.make_geometry(96, 16, 64)
+    monkeypatch.setenv("XCT_FMTD_EXACT", "1")
     monkeypatch.setenv("XCT_HOST_BUILD", "1")
     host = pipeline.assemble(g, pipeline.SystemConfig(precision=precision, ffactor=16,
                                                       build="monolithic"))
@@ -128,3 +190,11 @@ def test_streamed_device_build_equals_monolithic_host_build(precision, monkeypat
     y = rng.random((g.num_rays, 16)).astype(np.float32)
     assert np.array_equal(dev_sys.apply_forward(x)[0], host.apply_forward(x)[0])
     assert np.array_equal(dev_sys.apply_adjoint(y)[0], host.apply_adjoint(y)[0])
+    monkeypatch.delenv("XCT_FMTD_EXACT")
+    fast = pipeline.assemble(g, pipeline.SystemConfig(precision=precision, ffactor=16,
+                                                      build="streamed"))
+    for a, b in ((fast.apply_forward(x)[0], host.apply_forward(x)[0]),
+                 (fast.apply_adjoint(y)[0], host.apply_adjoint(y)[0])):
+        rel = float(np.linalg.norm(a - b) / np.linalg.norm(b))
+        print(f"{precision} fast schedule vs host: rel-L2 {rel:.2e}")
+        assert rel <= (1e-3 if precision == "mixed" else 5e-3)

@@ -94,3 +94,29 @@ def test_domain_exchange_plan_reassembles_the_operator():
 def O_transpose(ip, ix, v, n_rows, n_cols):
     from paper_2009_07226_b200.pipeline import _transpose
     return _transpose(ip, ix, v, n_rows, n_cols)
+
+
+def test_decompose_weighted_balances_siddon_work():
+    """Equal-nnz cuts of the Hilbert tile curve (SURVEY §7 hard part 3):
+    contiguous, complete, non-empty, and far better balanced than equal
+    tile counts for the column (voxel) work of a parallel-beam operator."""
+    import xct_oracle as O
+    from paper_2009_07226_b200 import hilbert
+    g = O.make_geom(64, 1, 64)
+    A = O.system_matrix(g)
+    w = np.bincount(A.indices, minlength=g.num_voxels).astype(np.float64)
+    grid = hilbert.TileGrid("tomogram", 64, 64, 8)
+    for P in (2, 4, 8):
+        eq = hilbert.decompose(grid, P)
+        wt = hilbert.decompose_weighted(grid, P, w)
+        assert np.array_equal(np.sort(np.concatenate([s.elements for s in wt])),
+                              np.arange(g.num_voxels))
+        assert all(len(s.tiles) > 0 for s in wt)
+        # contiguous along the curve: tiles in order, no gaps
+        order = [tuple(c) for c in hilbert.pseudo_hilbert_cells(grid.tiles_x, grid.tiles_z)]
+        assert [t for s in wt for t in s.tiles] == order
+        imb = lambda parts: max(w[s.elements].sum() for s in parts) / (w.sum() / P)
+        assert imb(wt) <= imb(eq) + 1e-9
+        # within one tile of perfect balance
+        tw = hilbert.tile_weights(grid, w)
+        assert imb(wt) <= 1.0 + P * tw.max() / w.sum()
