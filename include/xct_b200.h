@@ -176,10 +176,11 @@ typedef struct {
                                   schedule, (key, CSR position) order      */
   int32_t sched_fast;          /* 0: the host's schedule exactly (edge
                                   colouring by alternating paths, one thread
-                                  per quarter -- slow at scale); 1: first-fit
-                                  over step masks for slabs <= 64 steps
-                                  (same entries per row and slab, other
-                                  step placement)                          */
+                                  per quarter-warp); 1: that, and first fit
+                                  over step masks where a slab exceeds its
+                                  limits (> 256 steps); 2: first fit
+                                  everywhere (same entries per row and slab,
+                                  other step placement)                    */
 } xct_fmtd_part;
 
 int64_t xct_fmtd_scratch_bytes(void);

@@ -694,20 +694,26 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
       int ja_of[kRqMax];
       int ne = 0;
       bool over = false;
-      if (sched && p.fast && width <= 64) {
-        greedy_quarter<1>(a, T, tile, w, q, rq, rpw, width, k0, k1, gsb, so, scale,
-                          s_taken[threadIdx.x], wmax, nunder);
-        continue;
-      }
-      if (sched && p.fast && width <= 256) {
-        greedy_quarter<4>(a, T, tile, w, q, rq, rpw, width, k0, k1, gsb, so, scale,
-                          s_taken[threadIdx.x], wmax, nunder);
-        continue;
-      }
-      if (sched && p.fast && width <= 64 * kWideWords) {   // image-corner tiles, rare
-        uint64_t* scr = reinterpret_cast<uint64_t*>(S.atL);       // this thread's scratch
-        greedy_quarter_wide(a, T, tile, w, q, rq, rpw, width, k0, k1, gsb, so, scale, scr,
-                            scr + kRqMax * kWideWords, wmax, nunder);
+      // fast schedules: first fit over step masks (p.fast == 2 always; with
+      // p.fast == 1 only where the exact schedule does not fit its limits)
+      auto greedy = [&]() -> bool {
+        if (width <= 64) {
+          greedy_quarter<1>(a, T, tile, w, q, rq, rpw, width, k0, k1, gsb, so, scale,
+                            s_taken[threadIdx.x], wmax, nunder);
+        } else if (width <= 256) {
+          greedy_quarter<4>(a, T, tile, w, q, rq, rpw, width, k0, k1, gsb, so, scale,
+                            s_taken[threadIdx.x], wmax, nunder);
+        } else if (width <= 64 * kWideWords) {          // image-corner tiles, rare
+          uint64_t* scr = reinterpret_cast<uint64_t*>(S.atL);     // this thread's scratch
+          greedy_quarter_wide(a, T, tile, w, q, rq, rpw, width, k0, k1, gsb, so, scale, scr,
+                              scr + kRqMax * kWideWords, wmax, nunder);
+        } else {
+          return false;
+        }
+        return true;
+      };
+      if (sched && (p.fast == 2 || (p.fast == 1 && width > kNcMax))) {
+        if (!greedy()) atomicOr(a.flag, FLAG_SCHED);
         continue;
       }
       // edges: rows of the quarter in order, each row's group span in order
@@ -758,14 +764,20 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
       for (int e = 0; e < ne; ++e) ++cnt8[S.eslot[e] & cmask];
       int maxdeg = width;
       for (int c = 0; c < 8; ++c) maxdeg = max(maxdeg, cnt8[c]);
-      if (over || maxdeg > kNcMax || width > kNcMax) { atomicOr(a.flag, FLAG_SCHED); continue; }
+      if (over || maxdeg > kNcMax || width > kNcMax) {
+        if (!(p.fast && greedy())) atomicOr(a.flag, FLAG_SCHED);
+        continue;
+      }
       S.reset(rq, maxdeg);
       bool okc = true;
       for (int e = 0; e < ne && okc; ++e) {
         const int rr = S.er[e];
         okc = S.add(rr, S.eslot[e] & cmask);
       }
-      if (!okc) { atomicOr(a.flag, FLAG_SCHED); continue; }
+      if (!okc) {
+        if (!(p.fast && greedy())) atomicOr(a.flag, FLAG_SCHED);
+        continue;
+      }
       if (maxdeg != width) {
         for (int i = 0; i < rq * width; ++i) S.busy[i] = 0;
         for (int i = 0; i < width * 8; ++i) { S.ccnt[i] = 0; S.fslot[i] = -1; }
@@ -793,7 +805,10 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
           ++S.ccnt[best * 8 + c];
           if (S.fslot[best * 8 + c] < 0) S.fslot[best * 8 + c] = (int16_t)slot;
         }
-        if (!okc) { atomicOr(a.flag, FLAG_SCHED); continue; }
+        if (!okc) {
+          if (!(p.fast && greedy())) atomicOr(a.flag, FLAG_SCHED);
+          continue;
+        }
       }
       for (int n = 0; n < width; ++n) S.sslot[n] = -1;
       for (int i = 0; i < rq * width; ++i) S.used[i] = 0;
