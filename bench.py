@@ -361,6 +361,47 @@ def run_checks(args, cfg, g, system, y1, history, dev):
     return out
 
 
+def measure_exchange(run, system, ws, dev):
+    """NVLink traffic of the domain partition's exchanges: bytes each rank
+    sends per application (counted over the run) and the NCCL p2p time of
+    one extra CG iteration with the exchange phases serialized
+    (XCT_EXCHANGE_PROFILE=1, domain.py) -- GB/s per rank against NVLink 5's
+    900 GB/s per direction (nominal) and the pool's measured 770 GB/s peer
+    copy (B200_PROFILING.md).  Max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2009_07226_b200 import domain
+    bytes_run = {k: v["bytes_out_per_application"] for k, v in system.exchange_stats().items()}
+    for side in (system.forward, system.adjoint):
+        side.stats = domain._Stats()
+    os.environ["XCT_EXCHANGE_PROFILE"] = "1"
+    try:
+        run.step()
+    finally:
+        os.environ.pop("XCT_EXCHANGE_PROFILE", None)
+    st = system.exchange_stats()
+    out = {}
+    for name, v in st.items():
+        t = torch.tensor([v["nccl_seconds_per_application"],
+                          bytes_run.get(name, v["bytes_out_per_application"])],
+                         dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum)
+        sec, byt = float(tmax[0]), float(tmax[1])
+        gbs = byt / sec / 1e9 if sec > 0 else 0.0
+        out[name] = {"bytes_out_per_rank_max": byt, "bytes_total": float(tsum[1]),
+                     "nccl_ms_max": sec * 1e3, "gbs_per_rank": gbs,
+                     "frac_of_900_nominal": gbs / 900.0, "frac_of_770_measured": gbs / 770.0,
+                     "payload": "f32 partials" if name == "projection" else
+                                "normalized inputs at the storage dtype"}
+    out["note"] = ("NCCL p2p phase timed with the exchange serialized (one extra CG "
+                   "iteration, XCT_EXCHANGE_PROFILE=1); the timed run overlaps it with K6 in "
+                   f"{domain._Waves.WAVES} F-chunk waves")
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -394,7 +435,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     from paper_2009_07226_b200 import _lib, geometry, pipeline, solver
 
-    from paper_2009_07226_b200 import parallel
+    from paper_2009_07226_b200 import matrixstore, parallel
     scfg = pipeline.SystemConfig(precision=cfg["precision"], ffactor=16, order=args.order)
     # slices on this rank: weak scaling = a fixed group per GPU; strong
     # scaling = the config's total split by the reference's P_b rule
@@ -410,6 +451,13 @@ def main():
         S = cfg["slices"]
     t0 = time.perf_counter()
     system, t_matrix = None, 0.0
+    g = geometry.make_geometry(cfg["k"], S, cfg["n"])
+    # slice batch: with the device format build every GPU assembles its own
+    # copy of the operator in parallel; otherwise rank 0 builds on the host
+    # and broadcasts it over NVLink
+    own_build = not domain and (ws == 1 or (
+        pipeline._streamable(g, scfg) and
+        matrixstore.device_build_supported(pipeline.Plan_probe(scfg), scfg.precision)))
     if rank == 0:
         g, y1 = make_problem(cfg, S)
         t_matrix = time.perf_counter() - t0
@@ -417,8 +465,9 @@ def main():
             system = pipeline.assemble(g, scfg)
         geometry.clear_matrix_cache()
         torch.cuda.empty_cache()
-    else:
-        g = geometry.make_geometry(cfg["k"], S, cfg["n"])
+    elif own_build:
+        system = pipeline.assemble(g, scfg)
+        torch.cuda.empty_cache()
     if domain:
         import dataclasses
         scfg = dataclasses.replace(scfg, p_d=ws)
@@ -428,8 +477,9 @@ def main():
         dist.broadcast(yt, src=0)
         y1 = yt.cpu().numpy()
     elif ws > 1:
-        # one host build; the staged operator goes to every GPU over NVLink
-        system = parallel.broadcast_system(system, scfg, g)
+        if not own_build:
+            # one host build; the staged operator goes to every GPU over NVLink
+            system = parallel.broadcast_system(system, scfg, g)
         yt = (torch.from_numpy(y1).to(dev) if rank == 0 else
               torch.empty((g.num_rays, 1), dtype=torch.float64, device=dev))
         dist.broadcast(yt, src=0)
@@ -504,6 +554,9 @@ def main():
         traffic = json.loads(tf.read_text()).get("bytes_per_launch")
 
     history = list(run.result.residual_history)
+    exchange = None
+    if domain and getattr(system, "native", False):
+        exchange = measure_exchange(run, system, ws, dev)
     del run
     torch.cuda.empty_cache()
 
@@ -575,6 +628,8 @@ def main():
             "gpu_launches": launches,
             "e2e": e2e, "cpu_baseline": cpu, "checks": checks,
         }
+        if exchange is not None:
+            line["nvlink_exchange"] = exchange
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

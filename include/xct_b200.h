@@ -257,6 +257,8 @@ typedef struct {
   int32_t accumulate;     /* 1: out += result (rank-ordered partial sums) */
   const double* d_factors;/* [n_chunks] denormalize factors, NULL = 1     */
   double* d_dot_partials; /* [n_chunks*n_cta] sum of out^2, NULL = skip   */
+  int64_t x_chunk_stride; /* input records between F-chunks, 0 = n_in     */
+  int64_t x_elem_stride;  /* input records between elements, 0 = 1        */
 } xct_epilogue;
 
 int xct_spmm(const xct_staged* a, int precision, const void* d_x, int64_t n_in,
@@ -372,6 +374,19 @@ int xct_accumulate_rows(void* d_dst, int64_t n_dst, const void* d_src, const int
  * d_sumsq, the f64 sum of squares of the result (d_scratch[148*8]) */
 int xct_scale_chunks(void* d_v, int64_t per_chunk, int64_t n_chunks, const double* d_factors,
                      int f64, double* d_scratch, double* d_sumsq, void* stream);
+
+/* Element-major exchange buffers of the native domain partition
+ * ([m][n_chunks][record]: each peer's rows are one contiguous message):
+ * gather_records: dst[i][c] = src[c0 + c][idx[i]] (chunk-major source,
+ *   records of rec_bytes, a multiple of 16);
+ * accumulate_records: dst[c0 + c][pos[i]][f] += src[i][c][f] (f32/f64,
+ *   the caller orders the calls: owner first, then senders ascending). */
+int xct_gather_records(const void* d_src, int64_t n_src, const int32_t* d_idx, int64_t m,
+                       int64_t c0, int64_t n_chunks, int32_t rec_bytes, void* d_dst,
+                       void* stream);
+int xct_accumulate_records(void* d_dst, int64_t n_dst, int64_t c0, const void* d_src,
+                           const int32_t* d_pos, int64_t m, int64_t n_chunks, int32_t fd,
+                           int f64, void* stream);
 
 #ifdef __cplusplus
 }

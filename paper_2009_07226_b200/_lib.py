@@ -49,7 +49,8 @@ class FmtdPart(C.Structure):
 class Epilogue(C.Structure):
     _fields_ = [("d_out", vp), ("row_stride", i64), ("chunk_stride", i64),
                 ("valid_cols", i32), ("ffactor", i32), ("value_scale_exp", i32),
-                ("accumulate", i32), ("d_factors", vp), ("d_dot_partials", vp)]
+                ("accumulate", i32), ("d_factors", vp), ("d_dot_partials", vp),
+                ("x_chunk_stride", i64), ("x_elem_stride", i64)]
 
 
 _SIGS = {
@@ -92,6 +93,8 @@ _SIGS = {
     "xct_gather_rows": (i32, [vp, i64, vp, i64, i64, i32, i32, vp, vp]),
     "xct_accumulate_rows": (i32, [vp, i64, vp, vp, i64, i64, i32, i32, vp]),
     "xct_scale_chunks": (i32, [vp, i64, i64, vp, i32, vp, vp, vp]),
+    "xct_gather_records": (i32, [vp, i64, vp, i64, i64, i64, i32, vp, vp]),
+    "xct_accumulate_records": (i32, [vp, i64, i64, vp, vp, i64, i64, i32, i32, vp]),
 }
 
 _lib = None
@@ -146,7 +149,8 @@ KERNELS_PER_CALL = {"xct_dot": 2, "xct_sum_f64": 1, "xct_spmm": 1, "xct_maxabs":
                     "xct_accumulate_rows": 1, "xct_scale_chunks": 2,
                     "xct_rows_to_chunked": 2, "xct_unchunk_rows_f64": 1,
                     "xct_siddon_project_f32": 1, "xct_fmtd_ranges": 1, "xct_fmtd_count": 1,
-                    "xct_fmtd_fill": 1, "xct_csr_col_counts": 1}
+                    "xct_fmtd_fill": 1, "xct_csr_col_counts": 1,
+                    "xct_gather_records": 1, "xct_accumulate_records": 1}
 launch_count = [0]
 
 

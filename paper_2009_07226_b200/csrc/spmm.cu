@@ -43,6 +43,8 @@ struct Params {
   const void* values;
   const uint4* x;
   int64_t n_in;
+  int64_t x_chunk_pieces;   // 16-byte pieces between consecutive F-chunks of x
+  int32_t x_elem_pieces;    // 16-byte pieces between consecutive input elements
   int32_t rows_per_cta, warps_per_cta, log2_lanes, log2_pieces, n_cta;
   int32_t plane_slots;      // slots per shared-memory plane (multiple of 8)
   int32_t chunk_group;      // F-chunks of one tile scheduled back to back
@@ -292,9 +294,10 @@ __device__ __forceinline__ void stage_fill(const Params& p, const uint4* xb, uin
   const uint32_t dq = dst + plane_base(q, lp, p.plane_slots);
   const uint4* xq = xb + q;
   const int sstep = blockDim.x >> lp;
+  const uint32_t es = (uint32_t)p.x_elem_pieces;     // element offsets fit 32 bits
 #pragma unroll 1
   for (int s = threadIdx.x >> lp; s < ns; s += sstep)
-    cp_async16(dq + ((uint32_t)s << 4), xq + ((uint32_t)map[s] << lp), pol);
+    cp_async16(dq + ((uint32_t)s << 4), xq + (uint32_t)map[s] * es, pol);
 }
 
 // Copy the slot->element map of group g into shared memory (4-byte cp.async).
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(1024) spmm_staged_kernel(const Params p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rin = lane >> lg, sub = lane & ((1 << lg) - 1);
   const int row = p.cta_rows[(int64_t)b * p.rows_per_cta + warp * rpw + rin];
-  const uint4* xb = p.x + (int64_t)chunk * p.n_in * (1 << lp);
+  const uint4* xb = p.x + (int64_t)chunk * p.x_chunk_pieces;
   const uint64_t pol_x = policy_evict_last(), pol_e = policy_evict_first();
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(stage);
   const uint32_t bb = buffer_bytes(lp, p.plane_slots);
@@ -640,7 +643,7 @@ __global__ void __launch_bounds__(512) spmm_grouped_kernel(const Params p) {
   const int upw = 32 >> lg;                  // units per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int uin = lane >> lg, sub = lane & ((1 << lg) - 1);
-  const uint4* xb = p.x + (int64_t)chunk * p.n_in * (1 << lp);
+  const uint4* xb = p.x + (int64_t)chunk * p.x_chunk_pieces;
   const uint64_t pol_x = policy_evict_last(), pol_e = policy_evict_first();
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(stage);
   const uint32_t bb = buffer_bytes(lp, p.plane_slots);
@@ -925,6 +928,12 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   p.values = a->d_values;
   p.x = (const uint4*)d_x;
   p.n_in = n_in;
+  // input layout: chunk-major [n_chunks][n_in][record] unless the caller
+  // gives strides in records (e.g. element-major [n_in][n_chunks][record])
+  p.x_chunk_pieces = (ep->x_chunk_stride ? ep->x_chunk_stride : n_in) << lp;
+  p.x_elem_pieces = (int32_t)((ep->x_elem_stride ? ep->x_elem_stride : 1) << lp);
+  if ((uint64_t)n_in * (uint64_t)p.x_elem_pieces >= (1ull << 32))
+    return xct::fail(XCT_EINVAL, "spmm: input element offsets exceed 32 bits");
   p.rows_per_cta = (int32_t)a->rows_per_cta;
   p.warps_per_cta = (int32_t)a->warps_per_cta;
   p.log2_lanes = lg;

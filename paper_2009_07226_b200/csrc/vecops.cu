@@ -808,3 +808,65 @@ extern "C" int xct_unchunk_rows_f64(const void* d_in, int in_dtype, float fin, i
   XCT_CUDA_CHECK_LAUNCH("unchunk_rows_f64");
   return XCT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// K10 for the native domain partition (parallel.py): element-major exchange
+// buffers [m][n_chunks][record], so each peer's rows are ONE contiguous
+// NCCL message (footprints are ordered by owner) and no gather pass runs on
+// the K6 output side.
+namespace {
+__global__ void gather_records_k(const uint4* __restrict__ src, int64_t n_src,
+                                 const int32_t* __restrict__ idx, int64_t m, int64_t c0,
+                                 int64_t nc, int rp, uint4* __restrict__ dst) {
+  const int64_t total = m * nc * rp;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = t % rp, rc = t / rp;
+    const int64_t c = rc % nc, i = rc / nc;
+    dst[t] = src[((c0 + c) * n_src + idx[i]) * rp + q];
+  }
+}
+template <typename T>
+__global__ void accumulate_records_k(T* dst, int64_t n_dst, int64_t c0, const T* src,
+                                     const int32_t* pos, int64_t m, int64_t nc, int fd) {
+  const int64_t total = m * nc * fd;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = t % fd, rc = t / fd;
+    const int64_t c = rc % nc, i = rc / nc;
+    T* d = dst + ((c0 + c) * n_dst + pos[i]) * fd + f;
+    *d = *d + src[t];
+  }
+}
+}  // namespace
+
+extern "C" int xct_gather_records(const void* d_src, int64_t n_src, const int32_t* d_idx,
+                                  int64_t m, int64_t c0, int64_t n_chunks, int32_t rec_bytes,
+                                  void* d_dst, void* stream) {
+  if ((m && (!d_src || !d_idx || !d_dst)) || rec_bytes < 16 || rec_bytes % 16 || n_chunks < 0)
+    return xct::fail(XCT_EINVAL, "gather_records: bad argument");
+  const int64_t total = m * n_chunks * (rec_bytes / 16);
+  if (total == 0) return XCT_OK;
+  gather_records_k<<<blocks_for(total), kThreads, 0, (cudaStream_t)stream>>>(
+      (const uint4*)d_src, n_src, d_idx, m, c0, n_chunks, rec_bytes / 16, (uint4*)d_dst);
+  XCT_CUDA_CHECK_LAUNCH("gather_records");
+  return XCT_OK;
+}
+
+extern "C" int xct_accumulate_records(void* d_dst, int64_t n_dst, int64_t c0, const void* d_src,
+                                      const int32_t* d_pos, int64_t m, int64_t n_chunks,
+                                      int32_t fd, int f64, void* stream) {
+  if ((m && (!d_dst || !d_src || !d_pos)) || fd < 1 || n_chunks < 0)
+    return xct::fail(XCT_EINVAL, "accumulate_records: bad argument");
+  const int64_t total = m * n_chunks * fd;
+  if (total == 0) return XCT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (f64)
+    accumulate_records_k<double><<<blocks_for(total), kThreads, 0, s>>>(
+        (double*)d_dst, n_dst, c0, (const double*)d_src, d_pos, m, n_chunks, fd);
+  else
+    accumulate_records_k<float><<<blocks_for(total), kThreads, 0, s>>>(
+        (float*)d_dst, n_dst, c0, (const float*)d_src, d_pos, m, n_chunks, fd);
+  XCT_CUDA_CHECK_LAUNCH("accumulate_records");
+  return XCT_OK;
+}

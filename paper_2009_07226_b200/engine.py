@@ -65,17 +65,19 @@ _TUNE_GROUP = int(os.environ["XCT_SPMM_CHUNK_GROUP"]) if os.environ.get("XCT_SPM
 
 def apply_side(side: DeviceSide, x_chunked, out, *, row_stride: int, chunk_stride: int,
                valid_cols: int, ffactor_out: int, factors=None, dot_partials=None,
-               stream=None) -> None:
+               stream=None, x_chunk_stride: int = 0, x_elem_stride: int = 0) -> None:
     """Launch K6 on one staged side.
 
-    x_chunked: device tensor [n_chunks, n_in, f_dev] at the storage dtype.
+    x_chunked: device tensor [n_chunks, n_in, f_dev] at the storage dtype
+         (or any layout given by x_chunk_stride / x_elem_stride in records,
+         e.g. [n_in, n_chunks, f_dev]: x_chunk_stride=1, x_elem_stride=n_chunks).
     out: device f32 (f64 in double) tensor addressed as
          out[row*row_stride + chunk*chunk_stride + j], j < ffactor_out,
          chunk*ffactor_out + j < valid_cols.
     factors: f64 [n_chunks] denormalize factors; dot_partials: f64
          [n_chunks * n_cta] receives per-CTA sums of squares of the outputs.
     """
-    n_chunks = int(x_chunked.shape[0])
+    n_chunks = int(x_chunked.shape[1] if x_elem_stride else x_chunked.shape[0])
     ep = _lib.Epilogue()
     ep.d_out = out.data_ptr()
     ep.row_stride, ep.chunk_stride = int(row_stride), int(chunk_stride)
@@ -84,6 +86,7 @@ def apply_side(side: DeviceSide, x_chunked, out, *, row_stride: int, chunk_strid
     ep.accumulate = 0
     ep.d_factors = None if factors is None else factors.data_ptr()
     ep.d_dot_partials = None if dot_partials is None else dot_partials.data_ptr()
+    ep.x_chunk_stride, ep.x_elem_stride = int(x_chunk_stride), int(x_elem_stride)
     st = stream if stream is not None else _lib.stream_handle(x_chunked.device)
     if _TUNE_GROUP is not None:
         side.staged.chunk_group = _TUNE_GROUP

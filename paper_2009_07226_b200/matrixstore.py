@@ -773,6 +773,15 @@ def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int,
     return DevicePart(T, info, rows.reshape(-1), plan.kind)
 
 
+def host_part(hf: "HostFormat", precision: str, ffactor: int, n_in: int, n_out: int,
+              value_scale_exp: int, dev) -> DevicePart:
+    """A host-built part (e.g. grouped rows, which the device builder does
+    not make) uploaded and wrapped as a DevicePart for combine_device_parts."""
+    side = upload_format(hf, precision, ffactor, n_in, n_out, value_scale_exp, dev)
+    info = {f: getattr(side.info, f) for f in INFO_FIELDS}
+    return DevicePart(side.tensors, info, hf.cta_rows, hf.plan_kind)
+
+
 def combine_device_parts(parts: list, precision: str, ffactor: int, n_in: int, n_out: int,
                          value_scale_exp: int, dev) -> "DeviceSide":
     """Concatenate device-built parts over disjoint CTA tiles (offsets
@@ -799,7 +808,9 @@ def combine_device_parts(parts: list, precision: str, ffactor: int, n_in: int, n
                                        device=dev),
              "cta_rows": torch.empty(tot["n_cta"] * rpc, dtype=torch.int32, device=dev)}
         vt = parts[0].tensors["values"].dtype
-        T["values"] = torch.zeros(tot["n_padded"] + PAD_ENTRIES, dtype=vt, device=dev)
+        G = max(1, int(parts[0].info.get("row_group", 1)))
+        packed = packed and G == 1
+        T["values"] = torch.zeros((tot["n_padded"] + PAD_ENTRIES) * G, dtype=vt, device=dev)
         T["slots"] = (torch.zeros(1, dtype=torch.int16, device=dev) if packed else
                       torch.zeros(tot["n_padded"] + PAD_ENTRIES, dtype=torch.int16, device=dev))
         c_off = g_off = s_off = e_off = 0
@@ -814,7 +825,7 @@ def combine_device_parts(parts: list, precision: str, ffactor: int, n_in: int, n
             T["slab_off"][g_off * warps:(g_off + ng) * warps] = A["slab_off"][:ng * warps] + e_off
             T["slab_width"][g_off * warps:(g_off + ng) * warps] = A["slab_width"][:ng * warps]
             T["cta_rows"][c_off * rpc:(c_off + nc) * rpc] = A["cta_rows"][:nc * rpc]
-            T["values"][e_off:e_off + ne] = A["values"][:ne]
+            T["values"][e_off * G:(e_off + ne) * G] = A["values"][:ne * G]
             if not packed:
                 T["slots"][e_off:e_off + ne] = A["slots"][:ne]
             P.tensors = None               # release this part's device arrays

@@ -10,6 +10,7 @@ per rank, so host memory and build time do not scale with the GPU count.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -280,6 +281,10 @@ class DomainPartitionedSystem:
         self.config, self.geometry = config, geometry
         g = geometry
         self.num_rows, self.num_cols = g.num_rays, g.num_voxels
+        if config.order != "reference" and os.environ.get("XCT_DOMAIN_LEGACY") != "1":
+            self._init_native(g, config)
+            pipeline.configure_execution((self.forward, self.adjoint), config)
+            return
         tomo, sino = hilbert_subdomains(g, config.tile_size, self.world)
         self.col_owned = tomo[self.rank].elements
         self.row_owned = sino[self.rank].elements
@@ -370,6 +375,46 @@ class DomainPartitionedSystem:
         self.adjoint = _DistSide(mine[1], fp_adj[self.rank], self.col_owned, self.row_owned,
                                  fp_adj, [s.elements for s in tomo], self.rank, self.device)
         pipeline.configure_execution((self.forward, self.adjoint), config)
+
+    def _init_native(self, g, config):
+        """Native partition (domain.py): equal-nnz tomogram cut, per-rank
+        device build of A[:, T_r] and its transpose, owner-ordered
+        footprints, no gather on the K6 side of either exchange."""
+        import torch.distributed as dist
+        from . import domain
+        if config.precision not in ("single", "mixed", "half", "double"):
+            raise ValueError(f"unknown precision {config.precision!r}")
+        b = domain.NativeDomainBuild(g, config, self.rank, self.world, self.device)
+        fwd, adj, fp, seg, cols = b.run()
+        self.value_scale_exp = b.exp
+        self.tomogram_subdomains, self.sinogram_subdomains = b.tomo, b.sino
+        self.col_owned = cols
+        self.row_owned = b.sino[self.rank].elements
+        self.local_cols, self.local_rows = len(self.col_owned), len(self.row_owned)
+        box = [None] * self.world
+        dist.all_gather_object(box, (fp, seg))
+        fp_of, seg_of = [x[0] for x in box], [x[1] for x in box]
+        lists = domain.exchange_lists(fp_of, seg_of, self.row_owned, self.rank)
+        self.forward = domain.ForwardSide(fwd, seg, lists, self.local_rows, self.rank, self.world)
+        self.adjoint = domain.AdjointSide(adj, seg, lists, self.local_rows, self.rank, self.world)
+        own_rays = [s.elements for s in b.sino]
+        self.forward.footprints, self.forward.ownership = fp_of, own_rays
+        self.adjoint.footprints, self.adjoint.ownership = fp_of, own_rays
+        self.native = True
+        dist.barrier()
+
+    def exchange_stats(self) -> dict:
+        """Bytes this rank sent per application (and, under
+        XCT_EXCHANGE_PROFILE=1, the serialized NCCL time) for each side."""
+        out = {}
+        for name, side in (("projection", self.forward), ("backprojection", self.adjoint)):
+            st = getattr(side, "stats", None)
+            if st is None or not st.calls:
+                continue
+            out[name] = {"bytes_out_per_application": st.bytes_out / st.calls,
+                         "nccl_seconds_per_application": st.seconds / st.calls,
+                         "applications": st.calls}
+        return out
 
     def _init_streamed(self, g, config, tomo, sino):
         """Every rank builds its own blocks (no whole matrix anywhere)."""
