@@ -71,18 +71,22 @@ def broadcast_system(system, config, geometry, src: int = 0):
     import torch.distributed as dist
     rank = dist.get_rank()
     dev = torch.device("cuda", torch.cuda.current_device())
-    if rank == src and (len(system.forward.blocks) != 1 or
-                        system.forward.input_elements[0] is not None):
-        raise ValueError("broadcast_system supports the single-block (P_d = 1) operator")
     meta = [None]
     if rank == src:
-        m = system.matrix
-        meta = [dict(num_rows=int(m.num_rows), num_cols=int(m.num_cols), nnz=int(m.nnz),
-                     num_angles=int(getattr(m, "num_angles", m.num_rows)),
-                     num_detector_cols=int(getattr(m, "num_detector_cols", 1)),
-                     exp=int(system.value_scale_exp))]
+        if len(system.forward.blocks) != 1 or system.forward.input_elements[0] is not None:
+            # every rank must learn of the error, or the others block in the
+            # broadcast below
+            meta = [{"error": "broadcast_system supports the single-block (P_d = 1) operator"}]
+        else:
+            m = system.matrix
+            meta = [dict(num_rows=int(m.num_rows), num_cols=int(m.num_cols), nnz=int(m.nnz),
+                         num_angles=int(getattr(m, "num_angles", m.num_rows)),
+                         num_detector_cols=int(getattr(m, "num_detector_cols", 1)),
+                         exp=int(system.value_scale_exp))]
     dist.broadcast_object_list(meta, src=src, device=dev)
     meta = meta[0]
+    if "error" in meta:
+        raise ValueError(meta["error"])
     fwd = _bcast_side(system.forward.blocks[0] if rank == src else None, src, rank, dev)
     adj = _bcast_side(system.adjoint.blocks[0] if rank == src else None, src, rank, dev)
     if rank == src:
@@ -161,6 +165,14 @@ class _DistSide:
         self.rank, self.peers = rank, len(fp_of)
         self.footprints, self.ownership = fp_of, own_of   # all ranks' (volume_reports)
         t = lambda a: torch.as_tensor(np.asarray(a, np.int32), device=dev)
+        # send and receive sides pair rows by position in ascending element
+        # order: every footprint and ownership list must be strictly ascending
+        for name, arr in [("footprint", fp_ids), ("ownership", own_ids)] + \
+                [(f"footprint of rank {s}", f) for s, f in enumerate(fp_of)] + \
+                [(f"ownership of rank {s}", o) for s, o in enumerate(own_of)]:
+            a = np.asarray(arr)
+            if len(a) > 1 and not np.all(np.diff(a) > 0):
+                raise ValueError(f"{name} is not strictly ascending")
         owner = {}
         # positions of each peer's owned elements inside my footprint (send)
         self.send = {}
@@ -298,7 +310,25 @@ class DomainPartitionedSystem:
             self._init_streamed(g, config, tomo, sino)
             pipeline.configure_execution((self.forward, self.adjoint), config)
             return
+        err = None
         if self.rank == src:
+            try:
+                built, metas, exp = self._build_all(g, config, tomo, sino, rw, schedule)
+            except Exception as e:            # reported to every rank below
+                err = f"{type(e).__name__}: {e}"
+        box = [{"error": err} if err else metas]
+        dist.broadcast_object_list(box, src=src, device=self.device)
+        if isinstance(box[0], dict) and box[0].get("error"):
+            raise RuntimeError(f"domain build on rank {src} failed: {box[0]['error']}")
+        metas = box[0]
+        self._finish_legacy(g, config, tomo, sino, src, built if self.rank == src else None, metas)
+
+    def _build_all(self, g, config, tomo, sino, rw, schedule):
+        """Rank src: every rank's blocks from the whole matrix (legacy path,
+        reference order)."""
+        from . import geometry as geo
+        from .pipeline import column_block, row_block_transposed
+        if True:
             A = geo.build_system_matrix(g)
             ip, ix, v = A.host_csr32()
             exp = (matrixstore.half_rescale_exponent(v)
@@ -341,9 +371,11 @@ class DomainPartitionedSystem:
             geo.clear_matrix_cache()
             del A, ip, ix, v
             metas = [dict(exp=exp, f_fp=b[1], a_fp=b[2]) for b in built]
-        box = [metas]
-        dist.broadcast_object_list(box, src=src, device=self.device)
-        metas = box[0]
+        return built, metas, exp
+
+    def _finish_legacy(self, g, config, tomo, sino, src, built, metas):
+        import torch
+        from . import pipeline
         self.value_scale_exp = metas[0]["exp"]
         fp_fwd = [m["f_fp"] for m in metas]
         fp_adj = [m["a_fp"] for m in metas]

@@ -450,18 +450,67 @@ class AssembledSystem:
             engine.apply_side(blk, xp, pr, row_stride=n_chunks * F, chunk_stride=F,
                               valid_cols=n_chunks * F, ffactor_out=F, factors=None, stream=st)
             parts.append(pr.to(cd))
-        total = torch.zeros((side.num_outputs, n_chunks * F), dtype=cd, device=dev)
-        for q, own in enumerate(side.ownership):
-            keep = torch.zeros(side.num_outputs, dtype=torch.bool, device=dev)
-            keep[torch.as_tensor(own, device=dev)] = True
-            for s in [q] + [s for s in range(len(parts)) if s != q]:
-                rows = torch.as_tensor(side.footprints[s], device=dev)
-                hit = keep[rows]
-                total[rows[hit]] += parts[s][hit]
+        if cfg.comm_strategy == "hierarchical":
+            total = self._replay_hierarchical(side, parts, cd, n_chunks * F)
+        else:
+            total = torch.zeros((side.num_outputs, n_chunks * F), dtype=cd, device=dev)
+            for q, own in enumerate(side.ownership):
+                keep = torch.zeros(side.num_outputs, dtype=torch.bool, device=dev)
+                keep[torch.as_tensor(own, device=dev)] = True
+                for s in [q] + [s for s in range(len(parts)) if s != q]:
+                    rows = torch.as_tensor(side.footprints[s], device=dev)
+                    hit = keep[rows]
+                    total[rows[hit]] += parts[s][hit]
         odt = torch.float64 if cfg.precision == "double" else torch.float32
         f_cols = fac.to(odt).repeat_interleave(F)[None, :]
         res = total.to(odt) * f_cols
         out.copy_(res[:, :S])
+
+    def _replay_hierarchical(self, side, parts, cd, cols):
+        """The reference's execute_plan (src/comm.py:420-472) for the
+        hierarchical plan of this side (socket, node, then global level over
+        the configured topology): every level's transfers in sorted (sender,
+        receiver) order, the receiver adding each arriving contribution to
+        what it holds -- the same summation order as the reference, so
+        order="reference" results stay bit-identical with its default
+        comm_strategy.  (One process; dense per-process buffers, a
+        small-problem emulation path.)"""
+        import torch
+        dev, cfg = self.device, self.config
+        key = "projection" if side is self.forward else "backprojection"
+        plans = getattr(self, "_hier_plans", None)
+        if plans is None:
+            plans = self._hier_plans = {}
+        if key not in plans:
+            topo = cfg.topology if cfg.topology is not None else comm.default_topology()
+            placement = comm.map_partitions(cfg.p_b, cfg.p_d, topo)
+            eb = matrixstore.element_bytes(cfg.precision)
+            fps = {p: np.asarray(fp) for p, fp in enumerate(side.footprints)}
+            own = {q: np.asarray(o) for q, o in enumerate(side.ownership)}
+            plans[key] = comm.plan_hierarchical(fps, own, placement, ffactor=cfg.ffactor,
+                                                elem_bytes=eb)[0]
+        plan = plans[key]
+        n = side.num_outputs
+        P = max(len(parts), len(side.ownership))
+        vals = torch.zeros((P, n, cols), dtype=cd, device=dev)
+        has = torch.zeros((P, n), dtype=torch.bool, device=dev)
+        for p, part in enumerate(parts):
+            rows = torch.as_tensor(np.asarray(side.footprints[p]), device=dev)
+            vals[p, rows] = part
+            has[p, rows] = True
+        for level in plan.levels:
+            for (s_, r_) in sorted(level.transfers):
+                e = torch.as_tensor(np.asarray(level.transfers[(s_, r_)], np.int64), device=dev)
+                contrib = vals[s_, e]
+                has[s_, e] = False
+                prior = has[r_, e]
+                vals[r_, e] = torch.where(prior[:, None], vals[r_, e] + contrib, contrib)
+                has[r_, e] = True
+        total = torch.zeros((n, cols), dtype=cd, device=dev)
+        for q, own in enumerate(side.ownership):
+            o = torch.as_tensor(np.asarray(own, np.int64), device=dev)
+            total[o] = torch.where(has[q, o][:, None], vals[q, o], total[o])
+        return total
 
     # -- reporting ----------------------------------------------------------------
 
@@ -498,9 +547,12 @@ class AssembledSystem:
         (src/matrixstore.py:130-148 drops empty rows / untouched columns)."""
         m = self.matrix
         n_rows, n_cols = int(m.num_rows), int(m.num_cols)
+        rec = getattr(self, "_nonempty", None)
+        if rec is not None:                 # streamed build: recorded while building
+            return rec[name]
         ip, ix = getattr(m, "indptr", None), getattr(m, "indices", None)
-        if ip is None or ix is None:        # streamed build: no host CSR kept
-            return np.arange(n_rows if name == "projection" else n_cols)
+        if ip is None or ix is None:
+            raise ValueError("volume_reports needs the operator's non-empty rows/columns")
         if name == "projection":
             return np.flatnonzero(np.diff(np.asarray(ip)) > 0)
         return np.unique(np.asarray(ix))
@@ -641,6 +693,7 @@ class StreamedAssembly:
         return -int(math.floor(math.log2((big + small) / 2.0)))
 
     def _forward(self, exp):
+        import torch
         cfg, g = self.cfg, self.g
         n = g.grid_n
         ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta, cfg.row_group_effective)
@@ -654,6 +707,9 @@ class StreamedAssembly:
             plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - base, -1).astype(np.int32)
             tm.lap("plan")
             ip, ix, v = self._siddon(k0, k1)
+            self.ray_hit[k0 * n:k1 * n] = torch.diff(ip) > 0
+            _lib.call("xct_csr_col_counts", ip.data_ptr(), ix.data_ptr(), (k1 - k0) * n, 0,
+                      g.num_voxels, self.col_counts.data_ptr(), _lib.stream_handle(self.dev))
             ip, ix, v = self._d2h("f_ip", ip), self._d2h("f_ix", ix), self._d2h("f_v", v)
             tm.lap("siddon+d2h")
             hf = matrixstore.build_format(ip, ix, v, (k1 - k0) * n, g.num_voxels, plan,
@@ -765,6 +821,7 @@ class StreamedAssembly:
             rows = (k1 - k0) * n
             _lib.call("xct_csr_col_counts", ip.data_ptr(), ix.data_ptr(), rows, 0, g.num_voxels,
                       col_counts.data_ptr(), st)
+            self.ray_hit[k0 * n:k1 * n] = torch.diff(ip) > 0
             tm.lap("siddon")
             part = matrixstore.build_format_device(ip, ix, v, rows, g.num_voxels, plan,
                                                    cfg.precision, cfg.ffactor, exp,
@@ -849,14 +906,17 @@ class StreamedAssembly:
         chunks = self._chunks(ta)
         exp = self._exponent(chunks) if cfg.precision in ("half", "mixed") else 0
         self.nnz = 0
+        # outputs with at least one entry (the reference's footprints drop
+        # empty rays and untouched voxels, src/matrixstore.py:130-148)
+        self.ray_hit = torch.zeros(g.num_rays, dtype=torch.bool, device=self.dev)
+        self.col_counts = torch.zeros(g.num_voxels, dtype=torch.int64, device=self.dev)
         if self._device_ok():
             try:
-                counts = torch.zeros(g.num_voxels, dtype=torch.int64, device=self.dev)
-                fwd = self._forward_device(exp, counts)
-                adj = self._adjoint_device(exp, chunks, counts)
+                fwd = self._forward_device(exp, self.col_counts)
+                adj = self._adjoint_device(exp, chunks, self.col_counts)
                 info = MatrixInfo(g.num_rays, g.num_voxels, self.nnz, g.num_angles,
                                   g.num_detector_cols)
-                return AssembledSystem.from_sides(info, cfg, g, fwd, adj, exp)
+                return self._attach(AssembledSystem.from_sides(info, cfg, g, fwd, adj, exp))
             except matrixstore.DeviceBuildUnsupported as e:
                 _log(f"device format build declined ({e}); host builder")
                 self.nnz = 0
@@ -870,4 +930,10 @@ class StreamedAssembly:
         self._pool.clear()
         torch.cuda.empty_cache()
         info = MatrixInfo(g.num_rays, g.num_voxels, self.nnz, g.num_angles, g.num_detector_cols)
-        return AssembledSystem.from_sides(info, cfg, g, fwd, adj, exp)
+        return self._attach(AssembledSystem.from_sides(info, cfg, g, fwd, adj, exp))
+
+    def _attach(self, system):
+        system._nonempty = {
+            "projection": self.ray_hit.nonzero().reshape(-1).cpu().numpy(),
+            "backprojection": (self.col_counts > 0).nonzero().reshape(-1).cpu().numpy()}
+        return system

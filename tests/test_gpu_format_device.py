@@ -190,6 +190,11 @@ def test_streamed_device_build_equals_monolithic_host_build(precision, monkeypat
     y = rng.random((g.num_rays, 16)).astype(np.float32)
     assert np.array_equal(dev_sys.apply_forward(x)[0], host.apply_forward(x)[0])
     assert np.array_equal(dev_sys.apply_adjoint(y)[0], host.apply_adjoint(y)[0])
+    # the streamed build records its non-empty rays / touched voxels, so its
+    # exchange accounting equals the monolithic build's
+    from dataclasses import asdict
+    vd, vh = dev_sys.volume_reports(), host.volume_reports()
+    assert all(asdict(vd[k]) == asdict(vh[k]) for k in ("projection", "backprojection"))
     monkeypatch.delenv("XCT_FMTD_EXACT")
     fast = pipeline.assemble(g, pipeline.SystemConfig(precision=precision, ffactor=16,
                                                       build="streamed"))
