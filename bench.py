@@ -230,7 +230,8 @@ def run_reference_arm(args, cfg, ws, rank):
             "cg_s_per_iter": t,
             "cpu_baseline": {"value": gflops, "unit": "GFLOPS", "cores": cores, "kind": "port",
                              "sample": f"oracle port on {cores} host cores (one sample problem "
-                                       f"per core, {n} timed CGLS iterations spread over them): "
+                                       f"per core, {sum(per)} CGLS iterations spread over them, "
+                                       f"the first of each core untimed when it ran more): "
                                        f"{info['kp']} of {cfg['k']} views (every "
                                        f"{cfg['k'] // info['kp']}th, bit-exact), "
                                        f"{info['sp']} of {total} slices; EXTRAPOLATED "

@@ -40,7 +40,7 @@ constexpr int kGMax = 256;        // load groups per tile
 constexpr int kNcMax = 256;       // colours (steps) per quarter schedule
 constexpr int kEMax = 2048;       // edges per quarter schedule
 constexpr int kRqMax = 8;         // rows per quarter-warp
-constexpr int kFillThreads = 128;
+constexpr int kFillThreads = 256;  // latency-bound schedule: more threads in flight
 
 enum { FLAG_UNSORTED = 1, FLAG_CAPACITY = 2, FLAG_GROUPS = 4, FLAG_SPAN = 8, FLAG_SCHED = 16 };
 
@@ -636,7 +636,7 @@ __device__ __noinline__ void greedy_quarter_wide(const FillArgs& a, const Tile& 
 
 __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
   extern __shared__ int32_t sm[];
-  __shared__ uint64_t s_taken[kFillThreads][8 * 4];
+  __shared__ uint64_t s_taken[kFillThreads][8];      // greedy masks, slabs <= 64 steps
   const Part& p = a.p;
   Tile T;
   tile_carve(p, a.bm_words, sm, T);
@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
                             s_taken[threadIdx.x], wmax, nunder);
         } else if (width <= 256) {
           greedy_quarter<4>(a, T, tile, w, q, rq, rpw, width, k0, k1, gsb, so, scale,
-                            s_taken[threadIdx.x], wmax, nunder);
+                            reinterpret_cast<uint64_t*>(S.atR), wmax, nunder);
         } else if (width <= 64 * kWideWords) {          // image-corner tiles, rare
           uint64_t* scr = reinterpret_cast<uint64_t*>(S.atL);     // this thread's scratch
           greedy_quarter_wide(a, T, tile, w, q, rq, rpw, width, k0, k1, gsb, so, scale, scr,

@@ -354,8 +354,16 @@ __device__ __forceinline__ void run_group(A& acc, St (&r)[4], int n4, int64_t& a
   at += rem * step;
 }
 
+// 1024-thread bound (64 registers) where the accumulators are small (FP16
+// storage or FP32 with <= 2 pieces per lane: two 512-thread CTAs per SM);
+// 512 threads (128 registers) for the wide-record instantiations that
+// spilled under the 64-register cap (r01 VERDICT: staged<3,4>, <0,2>, <0,4>).
+template <int PREC, int NPL> struct StagedBound {
+  static constexpr int value = (PREC != XCT_DOUBLE && NPL <= 2) ? 1024 : 512;
+};
+
 template <int PREC, int NPL, bool CONTRACT>
-__global__ void __launch_bounds__(1024) spmm_staged_kernel(const Params p) {
+__global__ void __launch_bounds__(StagedBound<PREC, NPL>::value) spmm_staged_kernel(const Params p) {
   using A = Acc<PREC, NPL, CONTRACT>;
   using St = Step<PREC>;
   constexpr int V = A::V;
@@ -499,6 +507,8 @@ int launch(const Params& p, int64_t n_chunks, int threads, int64_t smem, cudaStr
   }
   const int64_t n_blocks = (int64_t)p.n_cta * n_chunks;
   if (n_blocks > 0x7fffffffLL) return xct::fail(XCT_EINVAL, "spmm: grid too large");
+  if (threads > StagedBound<PREC, NPL>::value)
+    return xct::fail(XCT_EINVAL, "spmm: too many threads per CTA for this record width");
   spmm_staged_kernel<PREC, NPL, CONTRACT><<<(unsigned)n_blocks, threads, smem, s>>>(p);
   XCT_CUDA_CHECK_LAUNCH("spmm_staged");
   return XCT_OK;
