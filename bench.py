@@ -362,7 +362,7 @@ def run_checks(args, cfg, g, system, y1, history, dev):
     return out
 
 
-def measure_exchange(run, system, ws, dev):
+def measure_exchange(run, system, ws, dev, k6_fwd_s=0.0):
     """NVLink traffic of the domain partition's exchanges: bytes each rank
     sends per application (counted over the run) and the NCCL p2p time of
     one extra CG iteration with the exchange phases serialized
@@ -382,6 +382,22 @@ def measure_exchange(run, system, ws, dev):
         os.environ.pop("XCT_EXCHANGE_PROFILE", None)
     st = system.exchange_stats()
     out = {}
+    fused = getattr(system.forward, "fused", False) and ws > 1
+    if fused and "projection" in st:
+        # fused exchange: the forward's peer rows leave as remote stores from
+        # K6's epilogue, overlapping the math; report the bytes and the rate
+        # they needed over the K6 time
+        v = st.pop("projection")
+        t = torch.tensor([bytes_run.get("projection", v["bytes_out_per_application"]),
+                          k6_fwd_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out["projection"] = {"mode": "fused: K6 epilogue stores into peers' receive buffers "
+                                     "(CUDA IPC over NVLink), no separate transfer phase",
+                             "bytes_out_per_rank_max": float(t[0]),
+                             "k6_forward_ms_max": float(t[1]) * 1e3,
+                             "gbs_per_rank_during_k6": float(t[0]) / float(t[1]) / 1e9
+                             if float(t[1]) > 0 else None,
+                             "payload": "f32 partials"}
     for name, v in st.items():
         t = torch.tensor([v["nccl_seconds_per_application"],
                           bytes_run.get(name, v["bytes_out_per_application"])],
@@ -557,7 +573,9 @@ def main():
     history = list(run.result.residual_history)
     exchange = None
     if domain and getattr(system, "native", False):
-        exchange = measure_exchange(run, system, ws, dev)
+        fwd = [e[1].elapsed_time(e[2]) / 1e3 for e in events if e[0]]
+        exchange = measure_exchange(run, system, ws, dev,
+                                    sum(fwd) / max(1, sum(1 for e in events if e[0])))
     del run
     torch.cuda.empty_cache()
 

@@ -259,6 +259,14 @@ typedef struct {
   double* d_dot_partials; /* [n_chunks*n_cta] sum of out^2, NULL = skip   */
   int64_t x_chunk_stride; /* input records between F-chunks, 0 = n_in     */
   int64_t x_elem_stride;  /* input records between elements, 0 = 1        */
+  /* fused exchange (native domain partition): when d_out_ptrs != NULL,
+   * output row r with d_seg[q] <= r < d_seg[q+1] is written at
+   * d_out_ptrs[q] + (r - d_seg[q]) * row_stride -- device pointers, peers'
+   * receive buffers mapped over NVLink (xct_ipc_open) or local; d_out is
+   * ignored.  d_out_ptrs [n_seg], d_seg [n_seg+1] in device memory. */
+  void* const* d_out_ptrs;
+  const int64_t* d_seg;
+  int32_t n_seg;
 } xct_epilogue;
 
 int xct_spmm(const xct_staged* a, int precision, const void* d_x, int64_t n_in,
@@ -374,6 +382,14 @@ int xct_accumulate_rows(void* d_dst, int64_t n_dst, const void* d_src, const int
  * d_sumsq, the f64 sum of squares of the result (d_scratch[148*8]) */
 int xct_scale_chunks(void* d_v, int64_t per_chunk, int64_t n_chunks, const double* d_factors,
                      int f64, double* d_scratch, double* d_sumsq, void* stream);
+
+/* CUDA IPC for the fused exchange: device memory this process allocates
+ * and exports (64-byte handle), and peers' exports mapped into this
+ * process (peer pointers usable by kernels over NVLink / NVSwitch). */
+int xct_ipc_alloc(int64_t bytes, void** d_ptr, void* h_handle /* [64] */);
+int xct_ipc_open(const void* h_handle /* [64] */, void** d_ptr);
+int xct_ipc_close(void* d_ptr);
+int xct_ipc_free(void* d_ptr);
 
 /* Element-major exchange buffers of the native domain partition
  * ([m][n_chunks][record]: each peer's rows are one contiguous message):

@@ -50,7 +50,8 @@ class Epilogue(C.Structure):
     _fields_ = [("d_out", vp), ("row_stride", i64), ("chunk_stride", i64),
                 ("valid_cols", i32), ("ffactor", i32), ("value_scale_exp", i32),
                 ("accumulate", i32), ("d_factors", vp), ("d_dot_partials", vp),
-                ("x_chunk_stride", i64), ("x_elem_stride", i64)]
+                ("x_chunk_stride", i64), ("x_elem_stride", i64), ("d_out_ptrs", vp),
+                ("d_seg", vp), ("n_seg", i32)]
 
 
 _SIGS = {
@@ -93,6 +94,10 @@ _SIGS = {
     "xct_gather_rows": (i32, [vp, i64, vp, i64, i64, i32, i32, vp, vp]),
     "xct_accumulate_rows": (i32, [vp, i64, vp, vp, i64, i64, i32, i32, vp]),
     "xct_scale_chunks": (i32, [vp, i64, i64, vp, i32, vp, vp, vp]),
+    "xct_ipc_alloc": (i32, [i64, C.POINTER(vp), vp]),
+    "xct_ipc_open": (i32, [vp, C.POINTER(vp)]),
+    "xct_ipc_close": (i32, [vp]),
+    "xct_ipc_free": (i32, [vp]),
     "xct_gather_records": (i32, [vp, i64, vp, i64, i64, i64, i32, vp, vp]),
     "xct_accumulate_records": (i32, [vp, i64, i64, vp, vp, i64, i64, i32, i32, vp]),
 }
@@ -150,7 +155,11 @@ KERNELS_PER_CALL = {"xct_dot": 2, "xct_sum_f64": 1, "xct_spmm": 1, "xct_maxabs":
                     "xct_rows_to_chunked": 2, "xct_unchunk_rows_f64": 1,
                     "xct_siddon_project_f32": 1, "xct_fmtd_ranges": 1, "xct_fmtd_count": 1,
                     "xct_fmtd_fill": 1, "xct_csr_col_counts": 1,
-                    "xct_gather_records": 1, "xct_accumulate_records": 1}
+                    "xct_ipc_alloc": (i32, [i64, C.POINTER(vp), vp]),
+    "xct_ipc_open": (i32, [vp, C.POINTER(vp)]),
+    "xct_ipc_close": (i32, [vp]),
+    "xct_ipc_free": (i32, [vp]),
+    "xct_gather_records": 1, "xct_accumulate_records": 1}
 launch_count = [0]
 
 

@@ -55,7 +55,54 @@ struct Params {
   int32_t valid_cols, ffactor, scale_exp;
   const double* factors;
   double* dot_partials;
+  // fused exchange: output row r of segment q (seg[q] <= r < seg[q+1]) goes
+  // to out_ptrs[q] + (r - seg[q]) * row_stride -- a peer GPU's receive
+  // buffer over NVLink (CUDA IPC mapping) or this GPU's own
+  void* const* out_ptrs;
+  const int64_t* seg;
+  int32_t n_seg;
 };
+
+// A row's NV f32 outputs starting at column j0: 16-byte vector stores when
+// the whole run is valid and aligned (fewer, larger transactions -- what
+// the fused exchange's remote NVLink stores need), else scalar stores.
+template <int NV, typename Fn>
+__device__ __forceinline__ void store_row(float* out, int j0, int chunk, const struct Params& p,
+                                          Fn val, double& sq) {
+  const bool full = j0 + NV <= p.ffactor && chunk * p.ffactor + j0 + NV <= p.valid_cols;
+  if (NV % 4 == 0 && full && ((reinterpret_cast<uintptr_t>(out + j0) & 15u) == 0)) {
+#pragma unroll
+    for (int i = 0; i < NV; i += 4) {
+      const float4 v = make_float4(val(i), val(i + 1), val(i + 2), val(i + 3));
+      *reinterpret_cast<float4*>(out + j0 + i) = v;
+      sq += (double)v.x * (double)v.x;      // same order as the scalar path
+      sq += (double)v.y * (double)v.y;
+      sq += (double)v.z * (double)v.z;
+      sq += (double)v.w * (double)v.w;
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int j = j0 + i;
+    if (j < p.ffactor && chunk * p.ffactor + j < p.valid_cols) {
+      const float v = val(i);
+      out[j] = v;
+      sq += (double)v * (double)v;
+    }
+  }
+}
+
+// destination row base of output row `row` (plain or segment-scattered)
+template <typename T>
+__device__ __forceinline__ T* out_row(const Params& p, int row, int chunk) {
+  if (!p.out_ptrs)
+    return (T*)p.out + (int64_t)row * p.row_stride + (int64_t)chunk * p.chunk_stride;
+  int q = 0;
+  while (q + 1 < p.n_seg && row >= p.seg[q + 1]) ++q;
+  return (T*)p.out_ptrs[q] + (int64_t)(row - p.seg[q]) * p.row_stride +
+         (int64_t)chunk * p.chunk_stride;
+}
 
 // ---- memory access helpers -------------------------------------------------
 // Entries stream through L2 once per F-chunk (evict_first); staged input
@@ -457,7 +504,7 @@ __global__ void __launch_bounds__(StagedBound<PREC, NPL>::value) spmm_staged_ker
     if constexpr (PREC == XCT_DOUBLE) {
       const double sc = ldexp(1.0, -p.scale_exp);
       const double f = p.factors ? p.factors[chunk] : 1.0;
-      double* out = (double*)p.out + (int64_t)row * p.row_stride + (int64_t)chunk * p.chunk_stride;
+      double* out = out_row<double>(p, row, chunk);
 #pragma unroll
       for (int i = 0; i < NPL * V; ++i) {
         const int j = j0 + i;
@@ -470,16 +517,8 @@ __global__ void __launch_bounds__(StagedBound<PREC, NPL>::value) spmm_staged_ker
     } else {
       const float sc = ldexpf(1.0f, -p.scale_exp);
       const float f = p.factors ? (float)p.factors[chunk] : 1.0f;
-      float* out = (float*)p.out + (int64_t)row * p.row_stride + (int64_t)chunk * p.chunk_stride;
-#pragma unroll
-      for (int i = 0; i < NPL * V; ++i) {
-        const int j = j0 + i;
-        if (j < p.ffactor && chunk * p.ffactor + j < p.valid_cols) {
-          const float v = acc.out(i, sc) * f;
-          out[j] = v;
-          sq += (double)v * (double)v;
-        }
-      }
+      float* out = out_row<float>(p, row, chunk);
+      store_row<NPL * V>(out, j0, chunk, p, [&](int i) { return acc.out(i, sc) * f; }, sq);
     }
   }
   if (p.dot_partials) {
@@ -808,16 +847,8 @@ done:
   for (int gi = 0; gi < G; ++gi) {
     const int row = p.cta_rows[(int64_t)b * p.rows_per_cta + (warp * upw + uin) * G + gi];
     if (row < 0) continue;
-    float* out = (float*)p.out + (int64_t)row * p.row_stride + (int64_t)chunk * p.chunk_stride;
-#pragma unroll
-    for (int i = 0; i < NPL * V; ++i) {
-      const int j = j0 + i;
-      if (j < p.ffactor && chunk * p.ffactor + j < p.valid_cols) {
-        const float v = acc[gi].out(i, sc) * f;
-        out[j] = v;
-        sq += (double)v * (double)v;
-      }
-    }
+    float* out = out_row<float>(p, row, chunk);
+    store_row<NPL * V>(out, j0, chunk, p, [&](int i) { return acc[gi].out(i, sc) * f; }, sq);
   }
   if (p.dot_partials) {
     for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
@@ -882,7 +913,8 @@ int launch_grouped_npl(const Params& p, int npl, int G, int64_t n_chunks, int th
 extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int64_t n_in,
                         int64_t n_chunks, int32_t f_dev, const xct_epilogue* ep,
                         int64_t smem_bytes, void* stream) {
-  if (!a || !ep || !d_x || !ep->d_out) return xct::fail(XCT_EINVAL, "spmm: null argument");
+  if (!a || !ep || !d_x || (!ep->d_out && !ep->d_out_ptrs))
+    return xct::fail(XCT_EINVAL, "spmm: null argument");
   if (precision < 0 || precision > 3) return xct::fail(XCT_EINVAL, "spmm: bad precision");
   if (ep->accumulate) return xct::fail(XCT_EINVAL, "spmm: accumulate mode is reserved");
   const int G = a->row_group > 1 ? a->row_group : 1;
@@ -960,6 +992,11 @@ extern "C" int xct_spmm(const xct_staged* a, int precision, const void* d_x, int
   p.scale_exp = ep->value_scale_exp;
   p.factors = ep->d_factors;
   p.dot_partials = ep->d_dot_partials;
+  p.out_ptrs = ep->d_out_ptrs;
+  p.seg = ep->d_seg;
+  p.n_seg = ep->n_seg;
+  if (p.out_ptrs && (!p.seg || p.n_seg < 1))
+    return xct::fail(XCT_EINVAL, "spmm: scattered output needs its segments");
   cudaStream_t s = (cudaStream_t)stream;
   if (G > 1) {
     if (precision == XCT_MIXED)

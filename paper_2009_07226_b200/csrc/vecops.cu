@@ -14,6 +14,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "xct_common.h"
 
@@ -868,5 +869,44 @@ extern "C" int xct_accumulate_records(void* d_dst, int64_t n_dst, int64_t c0, co
     accumulate_records_k<float><<<blocks_for(total), kThreads, 0, s>>>(
         (float*)d_dst, n_dst, c0, (const float*)d_src, d_pos, m, n_chunks, fd);
   XCT_CUDA_CHECK_LAUNCH("accumulate_records");
+  return XCT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// CUDA IPC (fused exchange of the native domain partition, domain.py)
+extern "C" int xct_ipc_alloc(int64_t bytes, void** d_ptr, void* h_handle) {
+  if (!d_ptr || !h_handle || bytes < 1) return xct::fail(XCT_EINVAL, "ipc_alloc: bad argument");
+  cudaError_t e = cudaMalloc(d_ptr, (size_t)bytes);
+  if (e != cudaSuccess) return xct::fail(XCT_ENOMEM, std::string("ipc_alloc: ") + cudaGetErrorString(e));
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, *d_ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*d_ptr);
+    *d_ptr = nullptr;
+    return xct::fail(XCT_ECUDA, std::string("ipc_alloc: handle: ") + cudaGetErrorString(e));
+  }
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(h_handle, &h, sizeof(h));
+  return XCT_OK;
+}
+
+extern "C" int xct_ipc_open(const void* h_handle, void** d_ptr) {
+  if (!d_ptr || !h_handle) return xct::fail(XCT_EINVAL, "ipc_open: bad argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, h_handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return xct::fail(XCT_ECUDA, std::string("ipc_open: ") + cudaGetErrorString(e));
+  return XCT_OK;
+}
+
+extern "C" int xct_ipc_close(void* d_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
+  if (e != cudaSuccess) return xct::fail(XCT_ECUDA, std::string("ipc_close: ") + cudaGetErrorString(e));
+  return XCT_OK;
+}
+
+extern "C" int xct_ipc_free(void* d_ptr) {
+  cudaError_t e = cudaFree(d_ptr);
+  if (e != cudaSuccess) return xct::fail(XCT_ECUDA, std::string("ipc_free: ") + cudaGetErrorString(e));
   return XCT_OK;
 }

@@ -96,8 +96,54 @@ class _Stats:
         self.calls = 0
 
 
+class IpcBuffer:
+    """Device memory this rank allocates and exports over CUDA IPC, and the
+    peers' exports mapped here (collective: every rank constructs one)."""
+
+    def __init__(self, nbytes: int, rank: int, world: int):
+        import ctypes as C
+        import torch.distributed as dist
+        L = _lib.lib()
+        handle = (C.c_char * 64)()
+        ptr = C.c_void_p()
+        _lib.check(L.xct_ipc_alloc(max(int(nbytes), 16), C.byref(ptr), handle), "xct_ipc_alloc")
+        self.ptr, self.nbytes = int(ptr.value), int(nbytes)
+        box = [None] * world
+        dist.all_gather_object(box, bytes(handle))
+        self.peer = {}
+        for q, h in enumerate(box):
+            if q == rank:
+                self.peer[q] = self.ptr
+                continue
+            pp = C.c_void_p()
+            _lib.check(L.xct_ipc_open(C.create_string_buffer(h, 64), C.byref(pp)), "xct_ipc_open")
+            self.peer[q] = int(pp.value)
+        self.rank = rank
+
+    def close(self):
+        L = _lib.lib()
+        for q, pt in self.peer.items():
+            if q != self.rank:
+                L.xct_ipc_close(pt)
+        L.xct_ipc_free(self.ptr)
+        self.peer = {}
+
+
+def fused_default() -> bool:
+    """The fused exchange (K6 epilogue stores into peers' buffers) is the
+    default; XCT_FUSED_EXCHANGE=0 selects the NCCL p2p waves."""
+    return os.environ.get("XCT_FUSED_EXCHANGE", "1") != "0"
+
+
 class ForwardSide:
-    """Projection on this rank: A[:, T_r] -> partials on F_r -> owners."""
+    """Projection on this rank: A[:, T_r] -> partials on F_r -> owners.
+
+    Fused exchange (default): K6's epilogue writes each footprint row owned
+    by peer q straight into q's receive buffer over NVLink (CUDA IPC
+    mapping, element-major [rows][chunks][F]), so the transfer runs tile by
+    tile inside the SpMM; a stream-ordered barrier (NCCL all-reduce of one
+    word) separates it from the owners' accumulation.  Same bytes, same
+    summation order as the NCCL p2p path (bit-identical results)."""
 
     def __init__(self, block, seg, lists, n_own_rows, rank, world):
         import torch
@@ -112,10 +158,84 @@ class ForwardSide:
         self.recv_pos = {s: t(p) for s, p in lists["recv_pos"].items()}
         self.stats = _Stats()
         self.footprints = self.ownership = None         # volume_reports: set by the system
+        self.fused = fused_default()
+        self._ipc = None
+        self._ipc_key = None
+
+    def setup_fused(self, recv_offsets_of):
+        """recv_offsets_of[q][s]: first row of sender s's block in rank q's
+        receive buffer (all ranks, from an all-gather)."""
+        self.recv_off_of = recv_offsets_of
+
+    def _fused_buffers(self, cg, C, fd, eb):
+        import torch
+        key = (C, fd, eb)
+        if self._ipc_key == key:
+            return
+        if self._ipc is not None:
+            self._ipc.close()
+        n_recv = sum(int(p.numel()) for p in self.recv_pos.values())
+        self._ipc = IpcBuffer(n_recv * C * fd * eb, self.rank, self.world)
+        a, b = self.seg[self.rank], self.seg[self.rank + 1]
+        self._own = torch.empty((max(b - a, 1), C, fd), dtype=cg.out_dt, device=cg.dev)
+        ptrs = []
+        for q in range(self.world):
+            if q == self.rank:
+                ptrs.append(self._own.data_ptr())
+            else:
+                off = self.recv_off_of[q].get(self.rank, 0)
+                ptrs.append(self._ipc.peer[q] + off * C * fd * eb)
+        self._ptrs = torch.tensor(ptrs, dtype=torch.int64, device=cg.dev)
+        self._seg = torch.tensor(self.seg, dtype=torch.int64, device=cg.dev)
+        self._flag = torch.zeros(1, dtype=torch.float32, device=cg.dev)
+        self._ipc_key = key
+
+    def _exchange_fused(self, cg, xin, out, fac) -> float:
+        import torch
+        import torch.distributed as dist
+        C, fd = cg.n_chunks, cg.f_dev
+        f64 = int(cg.out_dt == torch.float64)
+        eb = 8 if f64 else 4
+        self._fused_buffers(cg, C, fd, eb)
+        o = out.view(C, self.num_outputs, fd)
+        dist.all_reduce(self._flag)      # peers are done reading their buffers
+        ev = cg.events
+        if ev is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        engine.apply_side(self.block, xin, None, row_stride=C * fd, chunk_stride=fd,
+                          valid_cols=C * fd, ffactor_out=fd, factors=None, stream=cg.st,
+                          out_ptrs=self._ptrs, seg=self._seg)
+        if ev is not None:
+            e1.record()
+            ev.append((True, e0, e1, 1.0))
+        for q in range(self.world):
+            if q != self.rank:
+                self.stats.bytes_out += (self.seg[q + 1] - self.seg[q]) * C * fd * eb
+        dist.all_reduce(self._flag)      # every rank's K6 (and its remote stores) done
+        o.zero_()
+        a, b = self.seg[self.rank], self.seg[self.rank + 1]
+        _lib.call("xct_accumulate_records", o.data_ptr(), self.num_outputs, 0,
+                  self._own.data_ptr() if b > a else None, self.self_pos.data_ptr(), b - a, C,
+                  fd, f64, cg.st)
+        off = 0
+        for s in sorted(self.recv_pos):
+            pos = self.recv_pos[s]
+            _lib.call("xct_accumulate_records", o.data_ptr(), self.num_outputs, 0,
+                      self._ipc.ptr + off * C * fd * eb, pos.data_ptr(), pos.numel(), C, fd, f64,
+                      cg.st)
+            off += pos.numel()
+        self.stats.calls += 1
+        _lib.call("xct_scale_chunks", o.data_ptr(), self.num_outputs * fd, C, fac.data_ptr(), f64,
+                  cg.scratch.data_ptr(), cg.scal.data_ptr(), cg.st)
+        return float(cg.scal[0].item())
 
     def exchange_apply(self, cg, xin, out, fac) -> float:
         import torch
         import torch.distributed as dist
+        if self.fused and self.world > 1:
+            return self._exchange_fused(cg, xin, out, fac)
         C, fd = cg.n_chunks, cg.f_dev
         f64 = int(cg.out_dt == torch.float64)
         eb = 8 if f64 else 4

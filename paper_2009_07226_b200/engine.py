@@ -65,7 +65,8 @@ _TUNE_GROUP = int(os.environ["XCT_SPMM_CHUNK_GROUP"]) if os.environ.get("XCT_SPM
 
 def apply_side(side: DeviceSide, x_chunked, out, *, row_stride: int, chunk_stride: int,
                valid_cols: int, ffactor_out: int, factors=None, dot_partials=None,
-               stream=None, x_chunk_stride: int = 0, x_elem_stride: int = 0) -> None:
+               stream=None, x_chunk_stride: int = 0, x_elem_stride: int = 0,
+               out_ptrs=None, seg=None) -> None:
     """Launch K6 on one staged side.
 
     x_chunked: device tensor [n_chunks, n_in, f_dev] at the storage dtype
@@ -79,7 +80,7 @@ def apply_side(side: DeviceSide, x_chunked, out, *, row_stride: int, chunk_strid
     """
     n_chunks = int(x_chunked.shape[1] if x_elem_stride else x_chunked.shape[0])
     ep = _lib.Epilogue()
-    ep.d_out = out.data_ptr()
+    ep.d_out = out.data_ptr() if out is not None else None
     ep.row_stride, ep.chunk_stride = int(row_stride), int(chunk_stride)
     ep.valid_cols, ep.ffactor = int(valid_cols), int(ffactor_out)
     ep.value_scale_exp = int(side.value_scale_exp)
@@ -87,6 +88,8 @@ def apply_side(side: DeviceSide, x_chunked, out, *, row_stride: int, chunk_strid
     ep.d_factors = None if factors is None else factors.data_ptr()
     ep.d_dot_partials = None if dot_partials is None else dot_partials.data_ptr()
     ep.x_chunk_stride, ep.x_elem_stride = int(x_chunk_stride), int(x_elem_stride)
+    if out_ptrs is not None:       # fused exchange: rows scattered by segment
+        ep.d_out_ptrs, ep.d_seg, ep.n_seg = out_ptrs.data_ptr(), seg.data_ptr(), out_ptrs.numel()
     st = stream if stream is not None else _lib.stream_handle(x_chunked.device)
     if _TUNE_GROUP is not None:
         side.staged.chunk_group = _TUNE_GROUP

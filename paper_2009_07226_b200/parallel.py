@@ -428,6 +428,15 @@ class DomainPartitionedSystem:
         fp_of, seg_of = [x[0] for x in box], [x[1] for x in box]
         lists = domain.exchange_lists(fp_of, seg_of, self.row_owned, self.rank)
         self.forward = domain.ForwardSide(fwd, seg, lists, self.local_rows, self.rank, self.world)
+        # receive layout of the fused exchange: senders' blocks in ascending
+        # sender order, each rank's offsets known to all
+        offs, at = {}, 0
+        for s_ in sorted(lists["recv_pos"]):
+            offs[s_] = at
+            at += len(lists["recv_pos"][s_])
+        box2 = [None] * self.world
+        dist.all_gather_object(box2, offs)
+        self.forward.setup_fused(box2)
         self.adjoint = domain.AdjointSide(adj, seg, lists, self.local_rows, self.rank, self.world)
         own_rays = [s.elements for s in b.sino]
         self.forward.footprints, self.forward.ownership = fp_of, own_rays

@@ -69,6 +69,21 @@ def main(out_path, n=64, k=96, slices=5):
         if rank == 0:
             report[f"{prec}_streamed_equal"] = dict(equal=bool(np.array_equal(xs[0], xs[1])),
                                                     rel=rel(xs[1], xs[0]))
+    # native partition: the fused exchange (K6 epilogue stores into peers'
+    # buffers over CUDA IPC) and the NCCL p2p waves give identical results
+    for prec in ("single", "mixed"):
+        xs = []
+        for fused in ("1", "0"):
+            os.environ["XCT_FUSED_EXCHANGE"] = fused
+            cfg = pipeline.SystemConfig(precision=prec, ffactor=4, p_d=ws)
+            dps = parallel.DomainPartitionedSystem(g, cfg)
+            assert dps.forward.fused == (fused == "1")
+            res = solver.cgls_solve(dps, y, solver.SolveConfig(max_iters=4, precision=prec))
+            xs.append(dps.gather_x(res.x))
+        os.environ.pop("XCT_FUSED_EXCHANGE")
+        if rank == 0:
+            report[f"{prec}_fused_equal"] = dict(equal=bool(np.array_equal(xs[0], xs[1])),
+                                                 rel=rel(xs[1], xs[0]))
     if rank == 0:
         Path(out_path).write_text(json.dumps(report, indent=1))
         print(json.dumps(report, indent=1))

@@ -22,6 +22,7 @@ def test_domain_partitioned_operator_nccl(tmp_path):
     assert rep.pop("volume_reports_equal")     # partitioned == emulation byte accounting
     for prec in ("single", "mixed"):
         assert rep.pop(f"{prec}_streamed_equal")["equal"], prec
+        assert rep.pop(f"{prec}_fused_equal")["equal"], prec      # fused == NCCL p2p
     for key, r in rep.items():
         # reference staging + direct-plan reduction order: the NCCL exchange
         # reproduces the one-process emulation; only the cross-rank f64 dot
