@@ -295,7 +295,9 @@ class ForwardSide:
 
 class AdjointSide:
     """Back projection on this rank: inputs of F_r gathered from their
-    owners, then A[:, T_r]^T -> the owned voxels, complete."""
+    owners, then A[:, T_r]^T -> the owned voxels, complete.  Fused
+    (default): the owners' gather kernels store straight into this rank's
+    K6 input over NVLink; else NCCL p2p in F-chunk waves."""
 
     def __init__(self, block, seg, lists, n_own_rows, rank, world):
         import torch
@@ -310,10 +312,69 @@ class AdjointSide:
         self.send_idx = {q: t(p) for q, p in lists["send_idx"].items()}
         self.stats = _Stats()
         self.footprints = self.ownership = None
+        self.fused = fused_default()
+        self._ipc = None
+        self._ipc_key = None
+
+    def setup_fused(self, seg_of):
+        """seg_of[q]: rank q's owner segments of its footprint (where my
+        rays' records go in q's K6 input)."""
+        self.seg_of = [[int(v) for v in sg] for sg in seg_of]
+
+    def _exchange_fused(self, cg, xin, out, fac) -> float:
+        """Owners push their normalized inputs straight into the consumers'
+        K6 input buffers over NVLink: one gather kernel per consumer whose
+        destination is the consumer's buffer (CUDA IPC mapping) -- gather
+        and transfer in one pass, no NCCL staging; then K6 on the whole
+        element-major input."""
+        import torch
+        import torch.distributed as dist
+        C, fd = cg.n_chunks, cg.f_dev
+        eb = xin.element_size()
+        rec = fd * eb
+        key = (C, fd, eb)
+        if self._ipc_key != key:
+            if self._ipc is not None:
+                self._ipc.close()
+            self._ipc = IpcBuffer(self.n_fp * C * rec, self.rank, self.world)
+            self._flag = torch.zeros(1, dtype=torch.float32, device=cg.dev)
+            self._ipc_key = key
+        o = out.view(C, self.num_outputs, fd)
+        blk = self.block
+        parts = torch.empty(C * blk.info.n_cta, dtype=torch.float64, device=cg.dev)
+        dist.all_reduce(self._flag)           # consumers are done with their inputs
+        a, b = self.seg[self.rank], self.seg[self.rank + 1]
+        _lib.call("xct_gather_records", xin.data_ptr(), self.num_inputs, self.self_pos.data_ptr(),
+                  b - a, 0, C, rec, self._ipc.ptr + a * C * rec if b > a else None, cg.st)
+        for q, idx in self.send_idx.items():
+            dst = self._ipc.peer[q] + self.seg_of[q][self.rank] * C * rec
+            _lib.call("xct_gather_records", xin.data_ptr(), self.num_inputs, idx.data_ptr(),
+                      idx.numel(), 0, C, rec, dst, cg.st)
+            self.stats.bytes_out += idx.numel() * C * rec
+        dist.all_reduce(self._flag)           # every producer's stores landed
+        xfp = torch.empty(0, dtype=xin.dtype, device=cg.dev)
+        ev = cg.events
+        if ev is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        engine.apply_side_ptr(blk, self._ipc.ptr, C, o, row_stride=fd,
+                              chunk_stride=self.num_outputs * fd, valid_cols=C * fd,
+                              ffactor_out=fd, factors=fac, dot_partials=parts, stream=cg.st,
+                              x_chunk_stride=1, x_elem_stride=C)
+        if ev is not None:
+            e1.record()
+            ev.append((False, e0, e1, 1.0))
+        del xfp
+        self.stats.calls += 1
+        _lib.call("xct_sum_f64", parts.data_ptr(), parts.numel(), cg.scal.data_ptr(), cg.st)
+        return float(cg.scal[0].item())
 
     def exchange_apply(self, cg, xin, out, fac) -> float:
         import torch
         import torch.distributed as dist
+        if self.fused and self.world > 1:
+            return self._exchange_fused(cg, xin, out, fac)
         C, fd = cg.n_chunks, cg.f_dev
         rec = fd * xin.element_size()
         o = out.view(C, self.num_outputs, fd)

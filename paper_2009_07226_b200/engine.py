@@ -99,6 +99,19 @@ def apply_side(side: DeviceSide, x_chunked, out, *, row_stride: int, chunk_strid
     _lib.count_launches("xct_spmm")
 
 
+def apply_side_ptr(side: DeviceSide, x_ptr: int, n_chunks: int, out, **kw) -> None:
+    """apply_side on an input given as a raw device pointer (e.g. a CUDA IPC
+    receive buffer) of n_chunks F-chunks; layout by the x_* strides."""
+    class _X:                                   # the two attributes apply_side reads
+        shape = (side.n_in, n_chunks) if kw.get("x_elem_stride") else (n_chunks, side.n_in)
+        device = out.device
+
+        @staticmethod
+        def data_ptr():
+            return int(x_ptr)
+    apply_side(side, _X, out, **kw)
+
+
 def csr_spmm_f64(matrix, x: np.ndarray) -> np.ndarray:
     """y = A x in float64 on the device for a canonical CSR (host x)."""
     import torch

@@ -438,6 +438,7 @@ class DomainPartitionedSystem:
         dist.all_gather_object(box2, offs)
         self.forward.setup_fused(box2)
         self.adjoint = domain.AdjointSide(adj, seg, lists, self.local_rows, self.rank, self.world)
+        self.adjoint.setup_fused(seg_of)
         own_rays = [s.elements for s in b.sino]
         self.forward.footprints, self.forward.ownership = fp_of, own_rays
         self.adjoint.footprints, self.adjoint.ownership = fp_of, own_rays
