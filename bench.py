@@ -408,14 +408,19 @@ def measure_exchange(run, system, ws, dev, k6_fwd_s=0.0):
         dist.all_reduce(tsum)
         sec, byt = float(tmax[0]), float(tmax[1])
         gbs = byt / sec / 1e9 if sec > 0 else 0.0
-        out[name] = {"bytes_out_per_rank_max": byt, "bytes_total": float(tsum[1]),
+        out[name] = {"mode": ("fused: the owners' gather kernels store into the consumers' "
+                              "K6 inputs over NVLink (CUDA IPC); time = that phase, "
+                              "barriers included") if fused else "NCCL p2p, F-chunk waves",
+                     "bytes_out_per_rank_max": byt, "bytes_total": float(tsum[1]),
                      "nccl_ms_max": sec * 1e3, "gbs_per_rank": gbs,
                      "frac_of_900_nominal": gbs / 900.0, "frac_of_770_measured": gbs / 770.0,
                      "payload": "f32 partials" if name == "projection" else
                                 "normalized inputs at the storage dtype"}
-    out["note"] = ("NCCL p2p phase timed with the exchange serialized (one extra CG "
-                   "iteration, XCT_EXCHANGE_PROFILE=1); the timed run overlaps it with K6 in "
-                   f"{domain._Waves.WAVES} F-chunk waves")
+    out["note"] = ("times of one extra CG iteration with the exchange phases serialized "
+                   "(XCT_EXCHANGE_PROFILE=1); " + ("fused mode (default): the projection's "
+                   "transfer is inside K6" if fused else
+                   f"the timed run overlaps the NCCL p2p with K6 in {domain._Waves.WAVES} "
+                   "F-chunk waves"))
     return out
 
 

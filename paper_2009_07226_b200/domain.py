@@ -343,6 +343,11 @@ class AdjointSide:
         blk = self.block
         parts = torch.empty(C * blk.info.n_cta, dtype=torch.float64, device=cg.dev)
         dist.all_reduce(self._flag)           # consumers are done with their inputs
+        prof = os.environ.get("XCT_EXCHANGE_PROFILE") == "1"
+        if prof:
+            import time
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
         a, b = self.seg[self.rank], self.seg[self.rank + 1]
         _lib.call("xct_gather_records", xin.data_ptr(), self.num_inputs, self.self_pos.data_ptr(),
                   b - a, 0, C, rec, self._ipc.ptr + a * C * rec if b > a else None, cg.st)
@@ -352,6 +357,9 @@ class AdjointSide:
                       idx.numel(), 0, C, rec, dst, cg.st)
             self.stats.bytes_out += idx.numel() * C * rec
         dist.all_reduce(self._flag)           # every producer's stores landed
+        if prof:
+            torch.cuda.synchronize()
+            self.stats.seconds += time.perf_counter() - t0
         xfp = torch.empty(0, dtype=xin.dtype, device=cg.dev)
         ev = cg.events
         if ev is not None:
