@@ -619,7 +619,7 @@ def main():
         del x_host, res, y_host
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:      # N = 1 only
         r = cpu_baseline(cfg, S)
         cpu_gflops = flops_iter / r["t_iter_extrap"] / 1e9
         cpu = {"value": cpu_gflops, "unit": "GFLOPS", "cores": 1, "kind": "port",

@@ -41,14 +41,19 @@ def sha(a) -> str:
 
 def problem(n: int):
     """256: random-blobs (distinct slices, seed 0); 512: Shepp-Logan (every
-    slice identical, src/geometry.py:337-339 -- the fixture keeps one column)."""
+    slice identical, src/geometry.py:337-339 -- the fixture keeps one column);
+    128: config 1 itself (180 views, Shepp-Logan, float64 y)."""
     from xct import geometry
-    g = geometry.make_geometry(n, 16, n)
+    g = geometry.make_geometry(180 if n == 128 else n, 16, n)
     A = geometry.build_system_matrix(g)
+    if n == 128:
+        vol = geometry.generate_phantom("shepp-logan-like", n, 16)
+        y = geometry.simulate_measurements(A, vol, 0.0, 0).slices_as_columns()
+        return g, y, vol.slices_as_columns()
     kind = "random-blobs" if n == 256 else "shepp-logan-like"
     vol = geometry.generate_phantom(kind, n, 16, seed=0)
     y = geometry.simulate_measurements(A, vol, 0.0, 0).slices_as_columns()
-    return g, y.astype(np.float32), vol.slices_as_columns()
+    return g, y.astype(np.float32), vol.slices_as_columns()   # noqa
 
 
 def job(args):
@@ -77,13 +82,16 @@ def main(which: str = "all"):
         jobs += [(256, p, s, 30) for p in ("single", "mixed") for s in STAGINGS]
     if which in ("512", "all"):
         jobs += [(512, p, "default", 5) for p in ("single", "mixed")]
-    procs = 6 if which == "256" else 2
+    if which in ("128", "all"):          # config 1: the reference's own floor only
+        jobs += [(128, p, s, 30) for p in ("single", "mixed") for s in STAGINGS]
+    procs = 6 if which in ("256", "128") else 2
     with mp.get_context("fork").Pool(min(procs, len(jobs)), maxtasksperchild=1) as pool:
         runs = pool.map(job, jobs, chunksize=1)
     for n in sorted({r["n"] for r in runs}):
         _, y32, _ = problem(n)
         arrays, rec = {}, {"iters": None, "floor": {}}
         one_col = n == 512
+        keep_arrays = n != 128           # c1's arrays are in tests/golden/c1.npz
         arrays["y"] = y32[:, 0] if one_col else y32
         rec["y_sha"] = sha(y32)
         rec["phantom"] = "random-blobs seed 0" if n == 256 else "shepp-logan-like"
@@ -112,7 +120,8 @@ def main(which: str = "all"):
                     "curve_max_rel": float(np.max(np.abs(r["residual"] / base["residual"] - 1))),
                 } for r in alts}
         manifest[f"sub{n}"] = rec
-        np.savez_compressed(OUT / f"sub{n}.npz", **arrays)
+        if keep_arrays:
+            np.savez_compressed(OUT / f"sub{n}.npz", **arrays)
         print(f"sub{n}: floor {json.dumps(rec['floor'])}", flush=True)
     man_path.write_text(json.dumps(manifest, indent=1, sort_keys=True))
 
