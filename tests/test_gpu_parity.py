@@ -199,23 +199,23 @@ def test_c1_native_order_tolerances():
         assert rel_l2(res10.x, ref10["x"]) <= (1e-5 if prec == "single" else 2e-3), prec
         res = solver.cgls_solve(sysm, y, solver.SolveConfig(max_iters=30, precision=prec))
         curve = gold[f"cg_{prec}_residual"]
-        # the reference's own floor at config 1: its result moves this much
-        # when only its staging changes ((None,1) and (4 KiB,8) vs (96 KiB,4),
-        # tests/golden/sub_manifest.json "sub128"); the older
-        # random-order floor (noise_floor.json) only if that is absent
-        man = json.loads((GOLDEN / "sub_manifest.json").read_text()).get("sub128")
-        if man:
-            fl = man["floor"][prec]
-            floor_curve = max(v["curve_max_rel"] for v in fl.values())
-            floor_x = max(v["x_rel_l2"] for v in fl.values())
-        else:
-            floor_curve = max(floor[prec]["curve_max_rel"])
-            floor_x = max(floor[prec]["x_rel_l2"])
+        # the reference's own order-noise floor at config 1: how far its
+        # result moves when only the summation order changes -- its two other
+        # stagings ((None,1), (4 KiB,8) vs (96 KiB,4): tests/golden/
+        # sub_manifest.json "sub128") and the MEDIAN over five
+        # random valid per-row orders (noise_floor.json; the max, one outlier
+        # seed at 8.7%, made the r01 bound loose), whichever is larger
+        man = json.loads((GOLDEN / "sub_manifest.json").read_text())["sub128"]
+        fl = man["floor"][prec]
+        floor_curve = max(max(v["curve_max_rel"] for v in fl.values()),
+                          float(np.median(floor[prec]["curve_max_rel"])))
+        floor_x = max(max(v["x_rel_l2"] for v in fl.values()),
+                      float(np.median(floor[prec]["x_rel_l2"])))
         c_dev = float(np.max(np.abs(np.array(res.residual_history) / curve - 1)))
         x_dev = rel_l2(res.x, gold[f"cg_{prec}_x"])
         print(f"c1 {prec} native, 30 iterations: x rel-L2 {x_dev:.3e} (floor {floor_x:.3e}), "
               f"residual curve {c_dev:.3e} (floor {floor_curve:.3e})")
-        assert c_dev <= max(2 * floor_curve, 0.02 if prec == "mixed" else 0.0)
+        assert c_dev <= 2 * floor_curve
         assert x_dev <= 2 * floor_x
 
 
