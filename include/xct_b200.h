@@ -180,7 +180,12 @@ typedef struct {
                                   over step masks where a slab exceeds its
                                   limits (> 256 steps); 2: first fit
                                   everywhere (same entries per row and slab,
-                                  other step placement)                    */
+                                  other step placement); 3: paired half-
+                                  warp schedule where sched_rq == 8 (lanes
+                                  2k, 2k+1 read one record at merged steps:
+                                  one LDS wavefront per half-warp), first
+                                  fit per quarter elsewhere; d_qstats[2..3]
+                                  = merged / scheduled half-warp steps    */
 } xct_fmtd_part;
 
 int64_t xct_fmtd_scratch_bytes(void);

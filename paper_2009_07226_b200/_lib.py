@@ -14,7 +14,8 @@ from pathlib import Path
 import numpy as np
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libxct_b200.so"
+LIB_PATH = _HERE / ("libxct_b200_checked.so" if os.environ.get("XCT_LIB") == "checked"
+                     else "libxct_b200.so")
 
 XCT_OK, XCT_EINVAL, XCT_ECUDA, XCT_ESTAGE, XCT_ENOMEM, XCT_ENONFINITE = range(6)
 PREC_CODE = {"double": 0, "single": 1, "half": 2, "mixed": 3}

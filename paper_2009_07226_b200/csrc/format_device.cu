@@ -446,6 +446,8 @@ struct FillArgs {
 __device__ __forceinline__ void write_entry(const FillArgs& a, int64_t at, int slot, int64_t j,
                                             double scale, double& wmax, int64_t& nunder) {
   double v = 0.0, back = 0.0;
+  XCT_CHECK(slot >= 0 && slot < a.p.capacity && at >= 0);
+  XCT_CHECK(j < 0 || (j >= a.p.indptr[0] && j < a.p.indptr[a.p.n_rows]));
   if (j >= 0) v = a.p.values[j] * scale;
   if (a.precision == XCT_HALF || a.precision == XCT_MIXED) {
     uint32_t h = 0;
@@ -634,6 +636,306 @@ __device__ __noinline__ void greedy_quarter_wide(const FillArgs& a, const Tile& 
   }
 }
 
+// ---- paired half-warp schedule (sched mode 3) ------------------------------
+// A warp LDS.128 costs one shared-memory wavefront per half-warp (instead of
+// two) when each quarter of the half reads at most 4 distinct 16-byte
+// records and the half's records sit in distinct bank quads
+// (tools/smem_share_bench.cu: "pairs" 2.07 cycles vs 4.04 for 32 distinct
+// records).  With one lane per row, lanes (2k, 2k+1) of a half form pair k:
+// at a "merged" step both lanes read the same record -- a voxel (ray) both
+// rows touch, or one row's entry while its partner idles -- and the 8 pairs
+// read records of 8 distinct bank classes.  Per (group, warp, half):
+//   forced_k = max(0, n_a + n_b - shared_k - W) steps where pair k must read
+//   two records; F = max_k forced_k.  Steps [0, F) are scheduled per quarter
+//   as today (first fit over bank classes), pair k's doubles first; steps
+//   [F, W) are merged: the pairs' remaining tokens (shared entries and
+//   singles) are edge-coloured pairs x bank classes by the same alternating-
+//   path colourer as the quarter schedule (Sched), overflow of a class
+//   beyond W - F steps placed where it conflicts least.
+// Same entries per row and slab as every other schedule (only the steps
+// differ), so sums agree to rounding (native order).  Device-only: the host
+// builder has no such mode and stays the oracle for modes 0-2.
+constexpr int kPairW = kNcMax;
+struct PairScr {
+  int16_t *slot, *jo, *stp;   // [16][kPairW] per lane entry: slot, index in group span, step
+  int16_t *where;             // [4096] slot -> entry of lane b (-1 between uses)
+  int16_t *at;                // [16][kPairW] step -> slot read by the lane
+  int16_t *ta, *tb;           // [kEMax] merged-region token -> entry of lane a / b (-1: none)
+  int16_t *tu;                // [kEMax] edge -> entry being coloured
+  __device__ void carve(char* q) {
+    slot = (int16_t*)q; q += 16 * kPairW * 2;
+    jo = (int16_t*)q; q += 16 * kPairW * 2;
+    stp = (int16_t*)q; q += 16 * kPairW * 2;
+    where = (int16_t*)q; q += 4096 * 2;
+    at = (int16_t*)q; q += 16 * kPairW * 2;
+    ta = (int16_t*)q; q += kEMax * 2;
+    tb = (int16_t*)q; q += kEMax * 2;
+    tu = (int16_t*)q;
+  }
+  __host__ __device__ static constexpr int64_t bytes() {
+    return 4 * 16 * kPairW * 2 + 4096 * 2 + 3 * kEMax * 2;
+  }
+};
+
+__device__ __forceinline__ uint64_t step_bits(int k, int lo, int hi) {   // bits [lo,hi) of word k
+  const int a = max(lo - 64 * k, 0), b = min(hi - 64 * k, 64);
+  if (b <= a) return 0ull;
+  const uint64_t top = b == 64 ? ~0ull : ((1ull << b) - 1ull);
+  return top & ~((1ull << a) - 1ull);
+}
+__device__ __forceinline__ int first_bit(const uint64_t (&m)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (m[k]) return k * 64 + __ffsll((long long)m[k]) - 1;
+  return -1;
+}
+
+constexpr int64_t kFillScratch = Sched::bytes() + PairScr::bytes();   // per fill thread
+
+// Proper edge colouring of ne edges (row S.eidx[e] < nrows, bank class of
+// slot[ent[e]]) by the quarter schedule's alternating-path colourer with
+// max(ncol, class degree) colours; edges on colours >= ncol are the
+// overflow.  Returns the colour count used, -1 when it does not fit.
+__device__ int colour_core(Sched& S, int ne, int nrows, int ncol, const int16_t* ent,
+                           const int16_t* slot) {
+  if (ncol < 1) return -1;
+  int cnt8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int e = 0; e < ne; ++e) ++cnt8[slot[ent[e]] & 7];
+  int maxdeg = ncol;
+  for (int c = 0; c < 8; ++c) maxdeg = max(maxdeg, cnt8[c]);
+  if (maxdeg > kNcMax) return -1;
+  S.reset(nrows, maxdeg);
+  for (int e = 0; e < ne; ++e)
+    if (!S.add(S.eidx[e], slot[ent[e]] & 7)) return -1;
+  return maxdeg;
+}
+// Overflow edges (colour >= ncol; colour -2 = moved elsewhere, skipped)
+// onto the free step of their row where they conflict least.  Returns the
+// number of conflicting placements, -1 when a row has no free step.
+__device__ int place_overflow(Sched& S, int ne, int nrows, int ncol, const int16_t* ent,
+                              const int16_t* slot) {
+  bool any = false;
+  for (int e = 0; e < ne && !any; ++e) any = S.col[e] >= ncol;
+  if (!any) return 0;
+  int conflicts = 0;
+  for (int i = 0; i < nrows * ncol; ++i) S.busy[i] = 0;
+  for (int i = 0; i < ncol * 8; ++i) { S.ccnt[i] = 0; S.fslot[i] = -1; }
+  for (int e = 0; e < ne; ++e) {
+    const int c = S.col[e], cl = slot[ent[e]] & 7;
+    if (c < 0 || c >= ncol) continue;
+    S.busy[S.er[e] * ncol + c] = 1;
+    ++S.ccnt[c * 8 + cl];
+    if (S.fslot[c * 8 + cl] < 0) S.fslot[c * 8 + cl] = slot[ent[e]];
+  }
+  for (int e = 0; e < ne; ++e) {
+    if (S.col[e] < ncol) continue;
+    const int r = S.er[e], sl = slot[ent[e]], c = sl & 7;
+    int best = -1, best_cost = 1 << 30;
+    for (int st = 0; st < ncol; ++st) {
+      if (S.busy[r * ncol + st]) continue;
+      const int fs = S.fslot[st * 8 + c];
+      const int cost = fs < 0 || fs == sl ? 0 : S.ccnt[st * 8 + c];
+      if (cost < best_cost) { best_cost = cost; best = st; if (!cost) break; }
+    }
+    if (best < 0) return -1;
+    if (best_cost) ++conflicts;
+    S.col[e] = (int16_t)best;
+    S.busy[r * ncol + best] = 1;
+    ++S.ccnt[best * 8 + c];
+    if (S.fslot[best * 8 + c] < 0) S.fslot[best * 8 + c] = (int16_t)sl;
+  }
+  return conflicts;
+}
+
+// Returns false (nothing written) when the half does not fit the paired
+// schedule's limits; the caller then schedules its two quarters as usual.
+__device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int w, int h,
+                            int rpw, int W, int k0, int k1, int gsb, int64_t so, double scale,
+                            Sched& S, PairScr& P, double& wmax, int64_t& nunder,
+                            int64_t& merged) {
+  const Part& p = a.p;
+  if (W > kPairW || W < 1) return false;
+  int n[16];
+  int64_t ja[16];
+  for (int i = 0; i < 16; ++i) {
+    n[i] = 0;
+    ja[i] = 0;
+    const int32_t r = p.cta_rows[tile * p.rows_per_cta + w * rpw + h * 16 + i];
+    if (r < 0) continue;
+    const int64_t hi_j = p.indptr[r + 1];
+    int64_t L = p.indptr[r], H = hi_j;
+    while (L < H) {
+      const int64_t M = (L + H) >> 1;
+      int key, coord;
+      key_coord(T.mode, p.indices[M], p.B, key, coord);
+      if (key < k0) L = M + 1; else H = M;
+    }
+    ja[i] = L;
+    for (int64_t j = L; j < hi_j; ++j) {
+      int key, coord;
+      key_coord(T.mode, p.indices[j], p.B, key, coord);
+      if (key >= k1) break;
+      if (n[i] >= W) return false;
+      const int e = i * kPairW + n[i]++;
+      P.slot[e] = (int16_t)(bit_rank(T, T.kbase[key] + coord - T.lo[key]) - gsb);
+      P.jo[e] = (int16_t)(j - L);
+      P.stp[e] = -1;
+    }
+  }
+  // forced double steps per pair
+  int F = 0;
+  for (int k = 0; k < 8; ++k) {
+    const int A = 2 * k, B = A + 1;
+    for (int e = 0; e < n[B]; ++e) P.where[P.slot[B * kPairW + e]] = (int16_t)e;
+    int sh = 0;
+    for (int e = 0; e < n[A]; ++e) sh += P.where[P.slot[A * kPairW + e]] >= 0;
+    for (int e = 0; e < n[B]; ++e) P.where[P.slot[B * kPairW + e]] = -1;
+    F = max(F, n[A] + n[B] - sh - W);
+  }
+  const int M = W - F;
+  const bool minimal_u = p.fast == 4;
+  // per pair: which entries take the per-quarter steps [0, F) (marked -3),
+  // the rest become merged-region tokens (ta: lane a entry, tb: lane b
+  // entry, global indices lane * kPairW + e, -1: that lane idles)
+  int nt = 0;
+  int uc[16];                             // entries per lane on the per-quarter steps
+  for (int k = 0; k < 8; ++k) {
+    const int A = 2 * k, B = A + 1;
+    int16_t* sa = P.slot + A * kPairW;
+    int16_t* sb = P.slot + B * kPairW;
+    int16_t* pa = P.stp + A * kPairW;
+    int16_t* pb = P.stp + B * kPairW;
+    for (int e = 0; e < n[B]; ++e) P.where[sb[e]] = (int16_t)e;
+    int sh = 0;
+    for (int e = 0; e < n[A]; ++e)
+      if (P.where[sa[e]] >= 0) { ++sh; pb[P.where[sa[e]]] = -2; }   // B's copy of a shared entry
+    const int ua = n[A] - sh, ub = n[B] - sh;
+    // entries moved to the per-quarter steps: singles (alternating lanes),
+    // then shared pairs, until the pair's merged-region tokens fit the M
+    // merged steps (minimal; a slack of M/8 measured 0.7% slower at c5) or
+    // until [0, F) is full (fill)
+    const int tk0 = sh + ua + ub;
+    int need = minimal_u ? max(0, tk0 - M) : tk0;
+    int aU = 0, bU = 0, sU = 0;
+    while (need > 0) {
+      const bool ca_ok = aU < ua && aU + sU < F, cb_ok = bU < ub && bU + sU < F;
+      if (ca_ok && (aU <= bU || !cb_ok)) ++aU;
+      else if (cb_ok) ++bU;
+      else if (sU < sh && aU + sU < F && bU + sU < F) ++sU;
+      else break;
+      --need;
+    }
+    if (sU > sh || aU + sU > F || bU + sU > F) {
+      for (int e = 0; e < n[B]; ++e) P.where[sb[e]] = -1;
+      return false;
+    }
+    uc[A] = aU + sU;
+    uc[B] = bU + sU;
+    const int tk = sh - sU + (ua - aU) + (ub - bU);
+    if (tk > M || nt + tk > kEMax) {
+      for (int e = 0; e < n[B]; ++e) P.where[sb[e]] = -1;
+      return false;
+    }
+    int ca = 0, cb = 0, cs = 0;
+    for (int e = 0; e < n[A]; ++e) {
+      const int eb = P.where[sa[e]];
+      if (eb < 0) {
+        if (ca < aU) { pa[e] = -3; ++ca; }
+        else { P.ta[nt] = (int16_t)(A * kPairW + e); P.tb[nt] = -1; ++nt; }
+      } else if (cs < sU) {
+        pa[e] = -3; pb[eb] = -3; ++cs;
+      } else {
+        P.ta[nt] = (int16_t)(A * kPairW + e); P.tb[nt] = (int16_t)(B * kPairW + eb);
+        ++nt;
+      }
+    }
+    for (int e = 0; e < n[B]; ++e) {
+      if (pb[e] != -1) continue;          // shared (handled with A) or already placed
+      if (cb < bU) { pb[e] = -3; ++cb; }
+      else { P.ta[nt] = -1; P.tb[nt] = (int16_t)(B * kPairW + e); ++nt; }
+    }
+    for (int e = 0; e < n[B]; ++e) P.where[sb[e]] = -1;
+  }
+  // steps [F, W): pairs x bank classes edge-coloured with M colours; a
+  // class's overflow moves to the per-quarter steps where its lanes have
+  // room, else it takes the least-conflict free step of its pair
+  int conflicts = 0;
+  if (nt > 0) {
+    for (int e = 0; e < nt; ++e) {
+      P.tu[e] = P.ta[e] >= 0 ? P.ta[e] : P.tb[e];
+      S.eidx[e] = (int16_t)((P.tu[e] / kPairW) >> 1);
+    }
+    if (colour_core(S, nt, 8, M, P.tu, P.slot) < 0) return false;
+    for (int e = 0; e < nt; ++e) {
+      if (S.col[e] < M) continue;
+      const int ea = P.ta[e], eb = P.tb[e];
+      const int la = ea >= 0 ? ea / kPairW : -1, lb = eb >= 0 ? eb / kPairW : -1;
+      if ((la >= 0 && uc[la] >= F) || (lb >= 0 && uc[lb] >= F)) continue;
+      if (la >= 0) { P.stp[ea] = -3; ++uc[la]; }
+      if (lb >= 0) { P.stp[eb] = -3; ++uc[lb]; }
+      S.col[e] = -2;
+    }
+    conflicts = place_overflow(S, nt, 8, M, P.tu, P.slot);
+    if (conflicts < 0) return false;
+    for (int e = 0; e < nt; ++e) {
+      if (S.col[e] < 0) continue;
+      const int st = F + S.col[e];
+      if (P.ta[e] >= 0) P.stp[P.ta[e]] = (int16_t)st;
+      if (P.tb[e] >= 0) P.stp[P.tb[e]] = (int16_t)st;
+    }
+  }
+  // steps [0, F): per quarter, lanes x bank classes edge-coloured with F
+  // colours (the quarter schedule restricted to those steps)
+  for (int qq = 0; qq < 2; ++qq) {
+    int ne = 0;
+    for (int i = 8 * qq; i < 8 * qq + 8; ++i)
+      for (int e = 0; e < n[i]; ++e)
+        if (P.stp[i * kPairW + e] == -3) {
+          if (ne >= kEMax) return false;
+          P.tu[ne] = (int16_t)(i * kPairW + e);
+          S.eidx[ne] = (int16_t)(i & 7);
+          ++ne;
+        }
+    if (!ne) continue;
+    if (colour_core(S, ne, 8, F, P.tu, P.slot) < 0) return false;
+    if (place_overflow(S, ne, 8, F, P.tu, P.slot) < 0) return false;
+    for (int e = 0; e < ne; ++e) P.stp[P.tu[e]] = S.col[e];
+  }
+  // every entry on its own step of its lane (else nothing is written)
+  int16_t* at = P.at;                     // [16][W] step -> slot (-1 idle)
+  for (int i = 0; i < 16 * W; ++i) at[i] = -1;
+  for (int i = 0; i < 16; ++i)
+    for (int e = 0; e < n[i]; ++e) {
+      const int st = P.stp[i * kPairW + e];
+      if (st < 0 || st >= W || at[i * W + st] >= 0) return false;
+      at[i * W + st] = P.slot[i * kPairW + e];
+    }
+  // write: entries, then idle lanes re-read a record already read at that step
+  for (int i = 0; i < 16; ++i)
+    for (int e = 0; e < n[i]; ++e) {
+      const int st = P.stp[i * kPairW + e];
+      write_entry(a, so + ((int64_t)(st >> 2) * rpw + h * 16 + i) * 4 + (st & 3),
+                  P.slot[i * kPairW + e], ja[i] + P.jo[i * kPairW + e], scale, wmax, nunder);
+    }
+  for (int st = 0; st < W; ++st) {
+    for (int i = 0; i < 16; ++i) {
+      if (at[i * W + st] >= 0) continue;
+      int src = -1;
+      if (st >= F) {                      // merged: the partner, else any pair of the half
+        src = at[(i ^ 1) * W + st];
+        for (int o = 0; o < 16 && src < 0; ++o) src = at[o * W + st];
+      } else {                            // per quarter: the quarter's first busy lane
+        for (int o = i & 8; o < (i & 8) + 8 && src < 0; ++o) src = at[o * W + st];
+      }
+      if (src > 0)
+        write_entry(a, so + ((int64_t)(st >> 2) * rpw + h * 16 + i) * 4 + (st & 3), src, -1,
+                    scale, wmax, nunder);
+    }
+  }
+  merged += M - conflicts;
+  return true;
+}
+
 __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
   extern __shared__ int32_t sm[];
   __shared__ uint64_t s_taken[kFillThreads][8];      // greedy masks, slabs <= 64 steps
@@ -641,7 +943,15 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
   Tile T;
   tile_carve(p, a.bm_words, sm, T);
   Sched S;
-  S.carve(a.scratch + (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) * Sched::bytes());
+  PairScr P;
+  {
+    char* base = a.scratch + (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) * kFillScratch;
+    S.carve(base);
+    P.carve(base + Sched::bytes());
+    if (p.fast >= 3)
+      for (int i = 0; i < 4096; ++i) P.where[i] = -1;   // kept -1 between half jobs
+  }
+  int64_t merged = 0, half_steps = 0;
   const double scale = ldexp(1.0, a.scale_exp);
   const bool sched = p.rq > 1;
   const int rq = sched ? p.rq : 1;
@@ -680,6 +990,44 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
       a.group_map[sb + bit_rank(T, b)] = col_of(T.mode, lo_k, coord, p.B);
     }
     __syncthreads();
+    // paired half-warp schedule: one (group, warp, half) job per thread
+    if (p.fast >= 3 && rq == 8 && rpw % 16 == 0) {
+      const int nh = rpw / 16;
+      const int64_t hjobs = (int64_t)ng * W * nh;
+      for (int64_t job = threadIdx.x; job < hjobs; job += blockDim.x) {
+        const int h = (int)(job % nh);
+        const int w = (int)((job / nh) % W);
+        const int g = (int)(job / ((int64_t)nh * W));
+        const int width = T.width[g * W + w];
+        const int64_t so = a.slab_off[(gb + g) * W + w];
+        if (paired_half(a, T, tile, w, h, rpw, width, T.gk[g], T.gk[g + 1], T.gsb[g], so, scale,
+                        S, P, wmax, nunder, merged)) {
+          half_steps += width;
+          continue;
+        }
+        for (int q = 2 * h; q < 2 * h + 2; ++q) {
+          bool ok = true;
+          if (width <= 64)
+            greedy_quarter<1>(a, T, tile, w, q, rq, rpw, width, T.gk[g], T.gk[g + 1], T.gsb[g],
+                              so, scale, s_taken[threadIdx.x], wmax, nunder);
+          else if (width <= 256)
+            greedy_quarter<4>(a, T, tile, w, q, rq, rpw, width, T.gk[g], T.gk[g + 1], T.gsb[g],
+                              so, scale, reinterpret_cast<uint64_t*>(S.atR), wmax, nunder);
+          else if (width <= 64 * kWideWords) {
+            uint64_t* scr = reinterpret_cast<uint64_t*>(S.atL);
+            greedy_quarter_wide(a, T, tile, w, q, rq, rpw, width, T.gk[g], T.gk[g + 1],
+                                T.gsb[g], so, scale, scr, scr + kRqMax * kWideWords, wmax,
+                                nunder);
+          } else {
+            ok = false;
+          }
+          if (!ok) atomicOr(a.flag, FLAG_SCHED);
+        }
+        half_steps += width;
+      }
+      __syncthreads();
+      continue;
+    }
     // slabs: one (group, warp, quarter) job per thread at a time
     const int nq = rpw / rq;
     const int64_t jobs = (int64_t)ng * W * nq;
@@ -832,6 +1180,10 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
   }
   if (wmax > 0.0) atomicMax(&a.qstats[0], (unsigned long long)__double_as_longlong(wmax));
   if (nunder) atomicAdd(&a.qstats[1], (unsigned long long)nunder);
+  if (half_steps) {
+    atomicAdd(&a.qstats[2], (unsigned long long)merged);
+    atomicAdd(&a.qstats[3], (unsigned long long)half_steps);
+  }
 }
 
 int smem_ints(const Part& p, int bm_words) {
@@ -867,7 +1219,7 @@ int make_part(const xct_fmtd_part* in, Part& p) {
 }  // namespace
 
 extern "C" int64_t xct_fmtd_scratch_bytes(void) {
-  return (int64_t)148 * 2 * kFillThreads * Sched::bytes();
+  return (int64_t)148 * 2 * kFillThreads * kFillScratch;
 }
 
 extern "C" int xct_fmtd_ranges(const xct_fmtd_part* in, int32_t* d_lo, int32_t* d_hi,
@@ -917,7 +1269,7 @@ extern "C" int xct_fmtd_fill(const xct_fmtd_part* in, const int32_t* d_lo, const
   if (!d_values || (!packed && !d_slots) || !d_scratch)
     return xct::fail(XCT_EINVAL, "fmtd_fill: missing output arrays");
   const int64_t grid = std::min<int64_t>(p.n_cta, 148 * 2);
-  if (scratch_bytes < grid * kFillThreads * Sched::bytes())
+  if (scratch_bytes < grid * kFillThreads * kFillScratch)
     return xct::fail(XCT_EINVAL, "fmtd_fill: scratch too small");
   const size_t smem = (size_t)smem_ints(p, bm_words) * 4;
   if (smem > 227 * 1024) return xct::fail(XCT_ESTAGE, "fmtd_fill: tile footprint exceeds shared memory");

@@ -131,6 +131,7 @@ __global__ void siddon_fill_kernel(const double* __restrict__ cos_t,
     double* vp = values + base;
     trace(cos_t[k], sin_t[k], c, n_det, g, vox,
           [&](int64_t j, int32_t flat, double len) {
+            XCT_CHECK(j < rowptr[r + 1] - base && flat >= 0 && flat < g * g);
             ip[j] = flat;
             vp[j] = len;
           });

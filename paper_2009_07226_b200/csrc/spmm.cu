@@ -343,8 +343,10 @@ __device__ __forceinline__ void stage_fill(const Params& p, const uint4* xb, uin
   const int sstep = blockDim.x >> lp;
   const uint32_t es = (uint32_t)p.x_elem_pieces;     // element offsets fit 32 bits
 #pragma unroll 1
-  for (int s = threadIdx.x >> lp; s < ns; s += sstep)
+  for (int s = threadIdx.x >> lp; s < ns; s += sstep) {
+    XCT_CHECK((uint32_t)map[s] < (uint32_t)p.n_in && s < p.plane_slots);
     cp_async16(dq + ((uint32_t)s << 4), xq + (uint32_t)map[s] * es, pol);
+  }
 }
 
 // Copy the slot->element map of group g into shared memory (4-byte cp.async).
@@ -356,11 +358,13 @@ __device__ __forceinline__ void map_fill(const Params& p, int32_t* dst, int64_t 
 }
 
 template <int PREC, int NPL, typename A, typename St>
-__device__ __forceinline__ void consume(A& acc, const St& cur, const uint32_t (&pb)[NPL]) {
+__device__ __forceinline__ void consume(A& acc, const St& cur, const uint32_t (&pb)[NPL],
+                                        uint32_t lim) {
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const uint32_t off = cur.off(e);
     const auto len = cur.val(e);
+    XCT_CHECK(off < lim);
 #pragma unroll
     for (int qq = 0; qq < NPL; ++qq) acc.fma(qq, lds128(pb[qq] + off), len);
   }
@@ -373,29 +377,31 @@ __device__ __forceinline__ void run_group(A& acc, St (&r)[4], int n4, int64_t& a
                                           const int64_t step, const uint32_t (&pb)[NPL],
                                           const Params& p, uint64_t pol) {
   constexpr int S0 = P, S1 = (P + 1) & 3, S2 = (P + 2) & 3, S3 = (P + 3) & 3;
+  const uint32_t lim = 16u * (uint32_t)p.plane_slots;   // XCT_CHECK bound only
+  (void)lim;
   int k = 0;
   for (; k + 4 <= n4; k += 4) {
-    consume<PREC, NPL>(acc, r[S0], pb);
+    consume<PREC, NPL>(acc, r[S0], pb, lim);
     r[S0].load(p.slots, p.values, at, pol);
-    consume<PREC, NPL>(acc, r[S1], pb);
+    consume<PREC, NPL>(acc, r[S1], pb, lim);
     r[S1].load(p.slots, p.values, at + step, pol);
-    consume<PREC, NPL>(acc, r[S2], pb);
+    consume<PREC, NPL>(acc, r[S2], pb, lim);
     r[S2].load(p.slots, p.values, at + 2 * step, pol);
-    consume<PREC, NPL>(acc, r[S3], pb);
+    consume<PREC, NPL>(acc, r[S3], pb, lim);
     r[S3].load(p.slots, p.values, at + 3 * step, pol);
     at += 4 * step;
   }
   const int rem = n4 - k;
   if (rem >= 1) {
-    consume<PREC, NPL>(acc, r[S0], pb);
+    consume<PREC, NPL>(acc, r[S0], pb, lim);
     r[S0].load(p.slots, p.values, at, pol);
   }
   if (rem >= 2) {
-    consume<PREC, NPL>(acc, r[S1], pb);
+    consume<PREC, NPL>(acc, r[S1], pb, lim);
     r[S1].load(p.slots, p.values, at + step, pol);
   }
   if (rem >= 3) {
-    consume<PREC, NPL>(acc, r[S2], pb);
+    consume<PREC, NPL>(acc, r[S2], pb, lim);
     r[S2].load(p.slots, p.values, at + 2 * step, pol);
   }
   at += rem * step;
@@ -633,10 +639,12 @@ template <int G> struct GStep<XCT_MIXED, G> {
 };
 
 template <int NPL, int G, typename A, typename St>
-__device__ __forceinline__ void consume_g(A (&acc)[G], const St& cur, const uint32_t (&pb)[NPL]) {
+__device__ __forceinline__ void consume_g(A (&acc)[G], const St& cur, const uint32_t (&pb)[NPL],
+                                          uint32_t lim) {
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const uint32_t off = cur.off(e);
+    XCT_CHECK(off < lim);
 #pragma unroll
     for (int qq = 0; qq < NPL; ++qq) {
       const uint4 r = lds128(pb[qq] + off);
@@ -803,7 +811,7 @@ __global__ void __launch_bounds__(512) spmm_grouped_kernel(const Params p) {
     for (int64_t k = 0; k < total; ++k) {
       while (left == 0) enter(++g);
       if (k + 1 < total) fetch(k + 1, nxt);
-      consume_g<NPL, G>(acc, cur, pb);
+      consume_g<NPL, G>(acc, cur, pb, 16u * (uint32_t)p.plane_slots);
       __syncwarp();                     // every lane is done with ring slot k
       const int64_t kn = k + kBulkRing;
       if (lane == 0 && kn < total) {
@@ -827,7 +835,7 @@ __global__ void __launch_bounds__(512) spmm_grouped_kernel(const Params p) {
           if (++g >= g1) goto done;
           enter(g);
         }
-        consume_g<NPL, G>(acc, r[i], pb);
+        consume_g<NPL, G>(acc, r[i], pb, 16u * (uint32_t)p.plane_slots);
         r[i].load(lsp, lvp, upw, pol_e);
         lsp += step;
         lvp += vstep;

@@ -609,6 +609,7 @@ __global__ void gather_rows_k(const T* src, int64_t n_src, const int32_t* idx, i
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = t / (m * fd), rem = t % (m * fd);
     const int64_t i = rem / fd, f = rem % fd;
+    XCT_CHECK(idx[i] >= 0 && idx[i] < n_src);
     dst[t] = src[(c * n_src + idx[i]) * fd + f];
   }
 }
@@ -620,6 +621,7 @@ __global__ void accumulate_rows_k(T* dst, int64_t n_dst, const T* src, const int
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = t / (m * fd), rem = t % (m * fd);
     const int64_t i = rem / fd, f = rem % fd;
+    XCT_CHECK(pos[i] >= 0 && pos[i] < n_dst);
     T* d = dst + (c * n_dst + pos[i]) * fd + f;
     *d = *d + src[t];
   }
@@ -824,6 +826,7 @@ __global__ void gather_records_k(const uint4* __restrict__ src, int64_t n_src,
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t q = t % rp, rc = t / rp;
     const int64_t c = rc % nc, i = rc / nc;
+    XCT_CHECK(idx[i] >= 0 && idx[i] < n_src);
     dst[t] = src[((c0 + c) * n_src + idx[i]) * rp + q];
   }
 }
@@ -835,6 +838,7 @@ __global__ void accumulate_records_k(T* dst, int64_t n_dst, int64_t c0, const T*
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t f = t % fd, rc = t / fd;
     const int64_t c = rc % nc, i = rc / nc;
+    XCT_CHECK(pos[i] >= 0 && pos[i] < n_dst);
     T* d = dst + ((c0 + c) * n_dst + pos[i]) * fd + f;
     *d = *d + src[t];
   }

@@ -23,3 +23,21 @@ int fail(int code, const std::string& msg);
       return xct::fail(XCT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 #endif
+
+// XCT_CHECK(cond): a device-side bounds assertion in the checked build
+// (`make checked`, -DXCT_CHECKED): a failing check traps the kernel, which
+// surfaces as a CUDA error on the next call; compiled out otherwise.
+#ifdef __CUDACC__
+#ifdef XCT_CHECKED
+#define XCT_CHECK(cond)                                                                   \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("XCT_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                          \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define XCT_CHECK(cond) do {} while (0)
+#endif
+#endif

@@ -237,6 +237,12 @@ def forward_plan(num_angles: int, n: int, rows_per_warp: int, warps: int,
         n_ta, n_td = -(-(k1 - k0) // ta), -(-n // td)
         cells = pseudo_hilbert_cells(n_td, n_ta)           # (x = det tile, z = view tile)
         ai, di = np.divmod(np.arange(rpc), td)
+        if _paired_setting() == "all" and td == 32 and rw == 32 and ta % 2 == 0:
+            # view-paired lanes: warp = 2 views x 16 detectors, lanes (2k, 2k+1)
+            # = one detector in adjacent views (rays that share most voxels;
+            # the paired half-warp schedule merges their LDS reads)
+            w, ln = np.divmod(np.arange(rpc), 32)
+            ai, di = 2 * (w // 2) + (ln & 1), 16 * (w % 2) + ln // 2
     k = k0 + cells[:, 1:2] * ta + ai[None, :]
     c = cells[:, 0:1] * td + di[None, :]
     rows = np.where((k < k1) & (c < n), k * n + c, -1).astype(np.int32)
@@ -630,7 +636,6 @@ def upload_format(hf, precision: str, ffactor: int, n_in: int, n_out: int,
 # ---------------------------------------------------------------------------
 
 PAD_ENTRIES = 1024      # the kernel's load ring reads up to 4 steps past a slab
-_FMTD_SCRATCH = {}
 
 
 class DeviceBuildUnsupported(Exception):
@@ -650,14 +655,29 @@ def _sched_rq(plan: Plan, precision: str, ffactor: int, schedule: bool) -> int:
     return (8 >> lg) if lg <= 3 else 1
 
 
-def _sched_mode(exact: bool) -> int:
+def _paired_setting() -> str:
+    """XCT_FMTD_PAIRED: "adjoint" (default: the paired half-warp schedule
+    for A^T), "all" (also A, with view-paired forward lanes), "0" (off)."""
+    return os.environ.get("XCT_FMTD_PAIRED", "adjoint")
+
+
+def _sched_mode(exact: bool, kind: str = "forward") -> int:
     """0: the host's schedule exactly (raises where it cannot run); 1
     (default): the host's schedule, first fit where a slab exceeds its
     limits (image-corner tiles); 2: first fit everywhere (fastest build,
-    ~3% slower K6 at c5 from more bank conflicts, r02 measurement)."""
+    ~3% slower K6 at c5 from more bank conflicts, r02 measurement); 3/4:
+    the paired half-warp schedule (one LDS wavefront per half-warp where
+    row pairs share records; format_device.cu paired_half), 4 with only
+    the entries the merged steps cannot hold on the per-quarter steps (the
+    default for A^T; 3 fills those steps first)."""
     if exact or os.environ.get("XCT_FMTD_EXACT") == "1":
         return 0
-    return 2 if os.environ.get("XCT_FMTD_FAST") == "1" else 1
+    if os.environ.get("XCT_FMTD_FAST") == "1":
+        return 2
+    paired = _paired_setting()
+    if paired == "all" or (paired == "adjoint" and kind == "adjoint"):
+        return 3 if os.environ.get("XCT_FMTD_PAIRED_FILL") == "1" else 4
+    return 1
 
 
 @dataclass
@@ -701,7 +721,8 @@ def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int,
     part = _lib.FmtdPart(d_indptr.data_ptr(), d_indices.data_ptr(), d_values.data_ptr(),
                          int(n_rows), d_rows.data_ptr(), d_modes.data_ptr(), int(n_cta), int(rpc),
                          rpw, int(base_b), int(n_keys), int(capacity),
-                         _sched_rq(plan, precision, ffactor, schedule), _sched_mode(exact))
+                         _sched_rq(plan, precision, ffactor, schedule),
+                         _sched_mode(exact, plan.kind))
     i32, i64 = torch.int32, torch.int64
     flag = torch.zeros(1, dtype=i32, device=dev)
     lo = torch.empty(max(n_cta * n_keys, 1), dtype=i32, device=dev)
@@ -744,12 +765,10 @@ def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int,
         T["values"] = torch.zeros(n_padded + extra, dtype=torch.float64 if precision == "double"
                                   else torch.float32, device=dev)
         T["slots"] = torch.zeros(n_padded + extra, dtype=torch.int16, device=dev)
-    key = str(dev)
-    scratch = _FMTD_SCRATCH.get(key)
-    if scratch is None:
-        scratch = _FMTD_SCRATCH[key] = torch.empty(int(L.xct_fmtd_scratch_bytes()),
-                                                   dtype=torch.uint8, device=dev)
-    qs = torch.zeros(2, dtype=i64, device=dev)
+    # per call (the caching allocator hands the block back to later builds
+    # and, after assembly, to the solver's vectors)
+    scratch = torch.empty(int(L.xct_fmtd_scratch_bytes()), dtype=torch.uint8, device=dev)
+    qs = torch.zeros(4, dtype=i64, device=dev)
     d_base = torch.from_numpy(base).to(dev)
     _lib.check(L.xct_fmtd_fill(C.byref(part), lo.data_ptr(), hi.data_ptr(), bm_words,
                                widths.data_ptr(), d_base.data_ptr(), _lib.PREC_CODE[precision],
@@ -770,6 +789,8 @@ def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int,
                 value_bytes=element_bytes(precision),
                 max_rel_quant_error=float(q[:1].view(np.float64)[0]),
                 underflow_count=int(q[1]), row_group=1)
+    if q[3]:
+        info["paired_merged_steps"], info["paired_half_steps"] = int(q[2]), int(q[3])
     return DevicePart(T, info, rows.reshape(-1), plan.kind)
 
 

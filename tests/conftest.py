@@ -18,6 +18,11 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs through the CUDA C-ABI)")
 
 
+def pytest_report_header(config):
+    from paper_2009_07226_b200 import _lib
+    return f"xct library: {_lib.LIB_PATH.name}"
+
+
 @pytest.fixture(scope="session")
 def golden_manifest():
     return json.loads((GOLDEN / "manifest.json").read_text())

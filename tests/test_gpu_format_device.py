@@ -196,10 +196,93 @@ def test_streamed_device_build_equals_monolithic_host_build(precision, monkeypat
     vd, vh = dev_sys.volume_reports(), host.volume_reports()
     assert all(asdict(vd[k]) == asdict(vh[k]) for k in ("projection", "backprojection"))
     monkeypatch.delenv("XCT_FMTD_EXACT")
-    fast = pipeline.assemble(g, pipeline.SystemConfig(precision=precision, ffactor=16,
-                                                      build="streamed"))
-    for a, b in ((fast.apply_forward(x)[0], host.apply_forward(x)[0]),
-                 (fast.apply_adjoint(y)[0], host.apply_adjoint(y)[0])):
-        rel = float(np.linalg.norm(a - b) / np.linalg.norm(b))
-        print(f"{precision} fast schedule vs host: rel-L2 {rel:.2e}")
-        assert rel <= (1e-3 if precision == "mixed" else 5e-3)
+    for mode in ("0", "adjoint", "all"):
+        monkeypatch.setenv("XCT_FMTD_PAIRED", mode)
+        fast = pipeline.assemble(g, pipeline.SystemConfig(precision=precision, ffactor=16,
+                                                          build="streamed"))
+        for a, b in ((fast.apply_forward(x)[0], host.apply_forward(x)[0]),
+                     (fast.apply_adjoint(y)[0], host.apply_adjoint(y)[0])):
+            rel = float(np.linalg.norm(a - b) / np.linalg.norm(b))
+            print(f"{precision} paired={mode} schedule vs host: rel-L2 {rel:.2e}")
+            assert rel <= (1e-3 if precision == "mixed" else 5e-3)
+
+
+def _half_wavefronts(part, lanes_per_row=1):
+    """LDS.128 wavefronts per half-warp step under the measured rule
+    (tools/smem_share_bench.cu): one when each quarter reads <= 4 distinct
+    records and the half's distinct records sit in distinct bank classes,
+    else per quarter the worst class multiplicity.  Returns (wavefronts,
+    half-steps) over all slabs of a packed (half/mixed) format."""
+    T = {k: v.cpu().numpy() for k, v in part.tensors.items()}
+    rpw = int(part.info["rows_per_warp"])
+    slot = (T["values"].view(np.uint32) >> 20).astype(np.int64)
+    wf = hs = 0
+    for off, W in zip(T["slab_off"], T["slab_width"]):
+        if W == 0:
+            continue
+        st = np.arange(W)
+        at = off + (st[:, None] // 4) * rpw * 4 + np.arange(rpw)[None, :] * 4 + (st % 4)[:, None]
+        s = slot[at]                                   # [W, rpw]
+        for h in range(rpw // 16):
+            for n in range(W):
+                q0, q1 = set(s[n, 16 * h:16 * h + 8]), set(s[n, 16 * h + 8:16 * h + 16])
+                u = q0 | q1
+                if len(q0) <= 4 and len(q1) <= 4 and len({x & 7 for x in u}) == len(u):
+                    wf += 1
+                else:
+                    for q in (q0, q1):
+                        wf += max(sum(1 for x in q if x & 7 == c) for c in range(8))
+                hs += 1
+    return wf, hs
+
+
+@pytest.mark.parametrize("mode", ["min", "fill"])
+@pytest.mark.parametrize("kind", ["forward", "adjoint"])
+def test_paired_schedule_places_the_same_entries_and_merges(kind, mode, monkeypatch):
+    """Sched mode 3 (paired half-warp schedule): the same groups, maps,
+    widths and per-row slab entries as the host builder, fewer modelled
+    LDS wavefronts than the default schedule (K6 results: the streamed
+    test below)."""
+    k, n, precision = 180, 128, "mixed"
+    monkeypatch.setenv("XCT_FMTD_PAIRED", "all")          # view-paired forward lanes
+    g = geometry.make_geometry(k, 1, n)
+    A = geometry.build_system_matrix(g)
+    ip, ix, v = A.host_csr32()
+    cfg = pipeline.SystemConfig(precision=precision, ffactor=16, row_group=1)
+    rw = pipeline._rows_per_warp(cfg)
+    dev = geometry.device()
+    exp = matrixstore.half_rescale_exponent(np.asarray(v))
+    budget = cfg.smem_budget_effective
+    if kind == "forward":
+        a, b, c, nr, nc = ip, ix, v, g.num_rays, g.num_voxels
+        plan = matrixstore.assign_forward_regimes(
+            matrixstore.forward_plan(k, n, rw, cfg.warps_per_cta), g.angles, n)
+    else:
+        a, b, c = pipeline._transpose(ip, ix, v, g.num_rays, g.num_voxels)
+        nr, nc = g.num_voxels, g.num_rays
+        plan = matrixstore.adjoint_plan(k, n, rw, cfg.warps_per_cta)
+    hf = matrixstore.build_format(a, b, c, nr, nc, plan, precision, 16, exp, budget, schedule=True)
+    B, nk = pipeline.key_shape(g, kind)
+    args = (torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), torch.from_numpy(c).to(dev),
+            nr, nc, plan, precision, 16, exp, budget, True, B, nk, dev)
+    monkeypatch.setenv("XCT_FMTD_PAIRED", "0")
+    default = matrixstore.build_format_device(*args)
+    monkeypatch.setenv("XCT_FMTD_PAIRED", "all")
+    if mode == "fill":
+        monkeypatch.setenv("XCT_FMTD_PAIRED_FILL", "1")
+    paired = matrixstore.build_format_device(*args)
+    T = {k2: t.cpu().numpy() for k2, t in paired.tensors.items()}
+    for k2 in ("cta_group_ptr", "group_map_ptr", "group_map", "slab_off", "slab_width"):
+        assert np.array_equal(T[k2][:len(hf.arrays[k2])], hf.arrays[k2]), k2
+    ea = _row_entries(hf, hf.info, precision, True)
+    eb = _row_entries(paired, paired.info, precision, False)
+    assert len(ea) == len(eb)
+    assert all(np.array_equal(x, y) for x, y in zip(ea, eb))
+    assert paired.info["paired_half_steps"] > 0
+    wf_d, hs = _half_wavefronts(default)
+    wf_p, hs2 = _half_wavefronts(paired)
+    assert hs == hs2
+    print(f"{kind} mode {mode}: merged {paired.info['paired_merged_steps']} of "
+          f"{paired.info['paired_half_steps']} half-steps; modelled LDS wavefronts per "
+          f"half-step {wf_d / hs:.3f} (default) -> {wf_p / hs:.3f} (paired)")
+    assert wf_p < wf_d
