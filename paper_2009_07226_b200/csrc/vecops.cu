@@ -653,6 +653,7 @@ __global__ void gather_rows_v4(const float4* src, int64_t n_src, const int32_t* 
   float4* d = dst + (int64_t)c * total;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     const int i = t >> lq, q = t & ((1 << lq) - 1);
+    XCT_CHECK(idx[i] >= 0 && idx[i] < n_src);
     d[t] = s[((int64_t)idx[i] << lq) + q];
   }
 }
@@ -665,6 +666,7 @@ __global__ void accumulate_rows_v4(float4* dst, int64_t n_dst, const float4* src
   float4* d = dst + (int64_t)c * n_dst * (1 << lq);
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     const int i = t >> lq, q = t & ((1 << lq) - 1);
+    XCT_CHECK(pos[i] >= 0 && pos[i] < n_dst);
     float4* o = d + ((int64_t)pos[i] << lq) + q;
     float4 a = *o;
     const float4 b = s[t];
