@@ -185,7 +185,9 @@ typedef struct {
                                   2k, 2k+1 read one record at merged steps:
                                   one LDS wavefront per half-warp), first
                                   fit per quarter elsewhere; d_qstats[2..3]
-                                  = merged / scheduled half-warp steps    */
+                                  = merged / scheduled half-warp steps,
+                                  [4..5] = conflicting placements on the
+                                  per-quarter / merged steps             */
 } xct_fmtd_part;
 
 int64_t xct_fmtd_scratch_bytes(void);

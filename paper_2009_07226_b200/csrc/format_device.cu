@@ -752,7 +752,7 @@ __device__ int place_overflow(Sched& S, int ne, int nrows, int ncol, const int16
 __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int w, int h,
                             int rpw, int W, int k0, int k1, int gsb, int64_t so, double scale,
                             Sched& S, PairScr& P, double& wmax, int64_t& nunder,
-                            int64_t& merged) {
+                            int64_t& merged, int64_t& uconf, int64_t& mconf) {
   const Part& p = a.p;
   if (W > kPairW || W < 1) return false;
   int n[16];
@@ -792,8 +792,11 @@ __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int 
     for (int e = 0; e < n[B]; ++e) P.where[P.slot[B * kPairW + e]] = -1;
     F = max(F, n[A] + n[B] - sh - W);
   }
+  // extra per-quarter steps (slack for the tightest pair): pct of F, >= 1
+  const int extra_pct = (p.fast >> 8) & 0xff;
+  if (F > 0 && extra_pct) F = min(W, F + max(1, (F * extra_pct + 99) / 100));
   const int M = W - F;
-  const bool minimal_u = p.fast == 4;
+  const bool minimal_u = (p.fast & 0xff) == 4;
   // per pair: which entries take the per-quarter steps [0, F) (marked -3),
   // the rest become merged-region tokens (ta: lane a entry, tb: lane b
   // entry, global indices lane * kPairW + e, -1: that lane idles)
@@ -860,6 +863,11 @@ __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int 
   // class's overflow moves to the per-quarter steps where its lanes have
   // room, else it takes the least-conflict free step of its pair
   int conflicts = 0;
+  uint64_t mpair[8 * 4], mcls[8 * 4];     // merged steps taken per pair / per bank class
+  for (int i = 0; i < 32; ++i) { mpair[i] = 0ull; mcls[i] = 0ull; }
+  uint64_t mvalid[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) mvalid[k] = step_bits(k, 0, M);
   if (nt > 0) {
     for (int e = 0; e < nt; ++e) {
       P.tu[e] = P.ta[e] >= 0 ? P.ta[e] : P.tb[e];
@@ -882,6 +890,9 @@ __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int 
       const int st = F + S.col[e];
       if (P.ta[e] >= 0) P.stp[P.ta[e]] = (int16_t)st;
       if (P.tb[e] >= 0) P.stp[P.tb[e]] = (int16_t)st;
+      const int k = S.er[e], c = P.slot[P.tu[e]] & 7;
+      mpair[k * 4 + (S.col[e] >> 6)] |= 1ull << (S.col[e] & 63);
+      mcls[c * 4 + (S.col[e] >> 6)] |= 1ull << (S.col[e] & 63);
     }
   }
   // steps [0, F): per quarter, lanes x bank classes edge-coloured with F
@@ -898,8 +909,26 @@ __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int 
         }
     if (!ne) continue;
     if (colour_core(S, ne, 8, F, P.tu, P.slot) < 0) return false;
-    if (place_overflow(S, ne, 8, F, P.tu, P.slot) < 0) return false;
-    for (int e = 0; e < ne; ++e) P.stp[P.tu[e]] = S.col[e];
+    // a class's overflow takes a free merged step of its pair where its
+    // class is free (the partner idles there), else conflicts on [0, F)
+    for (int e = 0; e < ne; ++e) {
+      if (S.col[e] < F) continue;
+      const int k = (P.tu[e] / kPairW) >> 1, c = P.slot[P.tu[e]] & 7;
+      uint64_t m[4];
+#pragma unroll
+      for (int w4 = 0; w4 < 4; ++w4) m[w4] = mvalid[w4] & ~mpair[k * 4 + w4] & ~mcls[c * 4 + w4];
+      const int st = first_bit(m);
+      if (st < 0) continue;
+      mpair[k * 4 + (st >> 6)] |= 1ull << (st & 63);
+      mcls[c * 4 + (st >> 6)] |= 1ull << (st & 63);
+      P.stp[P.tu[e]] = (int16_t)(F + st);
+      S.col[e] = -2;
+    }
+    const int uc_q = place_overflow(S, ne, 8, F, P.tu, P.slot);
+    if (uc_q < 0) return false;
+    uconf += uc_q;
+    for (int e = 0; e < ne; ++e)
+      if (S.col[e] >= 0) P.stp[P.tu[e]] = S.col[e];
   }
   // every entry on its own step of its lane (else nothing is written)
   int16_t* at = P.at;                     // [16][W] step -> slot (-1 idle)
@@ -933,6 +962,7 @@ __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int 
     }
   }
   merged += M - conflicts;
+  mconf += conflicts;
   return true;
 }
 
@@ -948,10 +978,10 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
     char* base = a.scratch + (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) * kFillScratch;
     S.carve(base);
     P.carve(base + Sched::bytes());
-    if (p.fast >= 3)
+    if ((p.fast & 0xff) >= 3)
       for (int i = 0; i < 4096; ++i) P.where[i] = -1;   // kept -1 between half jobs
   }
-  int64_t merged = 0, half_steps = 0;
+  int64_t merged = 0, half_steps = 0, uconf = 0, mconf = 0;
   const double scale = ldexp(1.0, a.scale_exp);
   const bool sched = p.rq > 1;
   const int rq = sched ? p.rq : 1;
@@ -991,7 +1021,7 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
     }
     __syncthreads();
     // paired half-warp schedule: one (group, warp, half) job per thread
-    if (p.fast >= 3 && rq == 8 && rpw % 16 == 0) {
+    if ((p.fast & 0xff) >= 3 && rq == 8 && rpw % 16 == 0) {
       const int nh = rpw / 16;
       const int64_t hjobs = (int64_t)ng * W * nh;
       for (int64_t job = threadIdx.x; job < hjobs; job += blockDim.x) {
@@ -1001,7 +1031,7 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
         const int width = T.width[g * W + w];
         const int64_t so = a.slab_off[(gb + g) * W + w];
         if (paired_half(a, T, tile, w, h, rpw, width, T.gk[g], T.gk[g + 1], T.gsb[g], so, scale,
-                        S, P, wmax, nunder, merged)) {
+                        S, P, wmax, nunder, merged, uconf, mconf)) {
           half_steps += width;
           continue;
         }
@@ -1183,6 +1213,8 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
   if (half_steps) {
     atomicAdd(&a.qstats[2], (unsigned long long)merged);
     atomicAdd(&a.qstats[3], (unsigned long long)half_steps);
+    atomicAdd(&a.qstats[4], (unsigned long long)uconf);
+    atomicAdd(&a.qstats[5], (unsigned long long)mconf);
   }
 }
 

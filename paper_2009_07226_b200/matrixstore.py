@@ -676,7 +676,9 @@ def _sched_mode(exact: bool, kind: str = "forward") -> int:
         return 2
     paired = _paired_setting()
     if paired == "all" or (paired == "adjoint" and kind == "adjoint"):
-        return 3 if os.environ.get("XCT_FMTD_PAIRED_FILL") == "1" else 4
+        mode = 3 if os.environ.get("XCT_FMTD_PAIRED_FILL") == "1" else 4
+        extra = int(os.environ.get("XCT_FMTD_PAIRED_EXTRA", "20"))  # % of F, slack steps
+        return mode | (min(max(extra, 0), 255) << 8)
     return 1
 
 
@@ -768,7 +770,7 @@ def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int,
     # per call (the caching allocator hands the block back to later builds
     # and, after assembly, to the solver's vectors)
     scratch = torch.empty(int(L.xct_fmtd_scratch_bytes()), dtype=torch.uint8, device=dev)
-    qs = torch.zeros(4, dtype=i64, device=dev)
+    qs = torch.zeros(6, dtype=i64, device=dev)
     d_base = torch.from_numpy(base).to(dev)
     _lib.check(L.xct_fmtd_fill(C.byref(part), lo.data_ptr(), hi.data_ptr(), bm_words,
                                widths.data_ptr(), d_base.data_ptr(), _lib.PREC_CODE[precision],
@@ -791,6 +793,7 @@ def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int,
                 underflow_count=int(q[1]), row_group=1)
     if q[3]:
         info["paired_merged_steps"], info["paired_half_steps"] = int(q[2]), int(q[3])
+        info["paired_conflicts"] = {"quarter_steps": int(q[4]), "merged_steps": int(q[5])}
     return DevicePart(T, info, rows.reshape(-1), plan.kind)
 
 
