@@ -15,14 +15,15 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2009_07226_b200 import geometry, pipeline
 n = int(os.environ.get("N", "1024"))
-g = geometry.make_geometry(n, 16, n)
+S = int(os.environ.get("S", "16"))
+g = geometry.make_geometry(n, S, n)
 rng = np.random.default_rng(0)
-x = rng.random((g.num_voxels, 16)).astype(np.float32)
-y = rng.random((g.num_rays, 16)).astype(np.float32)
+x = rng.random((g.num_voxels, S)).astype(np.float32)
+y = rng.random((g.num_rays, S)).astype(np.float32)
 for mode in os.environ.get("MODES", "0 adjoint all").split():
     os.environ["XCT_FMTD_PAIRED"] = mode
     s = pipeline.assemble(g, pipeline.SystemConfig(precision="mixed", ffactor=16))
-    for _ in range(2):
+    for _ in range(int(os.environ.get("REPS", "2"))):
         s.apply_adjoint(y)
         s.apply_forward(x)
     torch.cuda.synchronize()
