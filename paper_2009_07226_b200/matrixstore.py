@@ -27,6 +27,7 @@ power of two in [16, 512] bytes; one lane owns 16 bytes of it.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 import os
 from dataclasses import dataclass, field
@@ -246,10 +247,25 @@ def forward_plan(num_angles: int, n: int, rows_per_warp: int, warps: int,
     k = k0 + cells[:, 1:2] * ta + ai[None, :]
     c = cells[:, 0:1] * td + di[None, :]
     rows = np.where((k < k1) & (c < n), k * n + c, -1).astype(np.int32)
-    cols = np.arange(n * n, dtype=np.int64)
-    iz, ix = np.divmod(cols, n)
-    tables = np.stack([iz, ix, n - 1 - ix]).astype(np.int32)
-    return Plan(rows, tables, np.zeros(len(rows), np.int32), rw, "forward", row_group)
+    return Plan(rows, _forward_key_tables(n), np.zeros(len(rows), np.int32), rw, "forward",
+                row_group)
+
+
+@functools.lru_cache(maxsize=4)
+def _forward_key_tables(n: int) -> np.ndarray:
+    """Band keys of every voxel column (z, x ascending, x descending); the
+    same for every chunk of views, so built once (read-only)."""
+    iz, ix = np.divmod(np.arange(n * n, dtype=np.int64), n)
+    t = np.stack([iz, ix, n - 1 - ix]).astype(np.int32)
+    t.flags.writeable = False
+    return t
+
+
+@functools.lru_cache(maxsize=4)
+def _adjoint_key_tables(num_angles: int, n: int) -> np.ndarray:
+    t = (np.arange(num_angles * n, dtype=np.int64) // n).astype(np.int32)[None, :]
+    t.flags.writeable = False
+    return t
 
 
 def forward_tile_height(n: int, rows_per_warp: int, warps: int, row_group: int = 1) -> int:
@@ -310,8 +326,8 @@ def adjoint_plan(num_angles: int, n: int, rows_per_warp: int, warps: int,
     z = z0 + cells[:, 1:2] * tz + zi[None, :]
     x = cells[:, 0:1] * tx + xi[None, :]
     rows = np.where((z < z1) & (x < n), z * n + x, -1).astype(np.int32)
-    tables = (np.arange(num_angles * n, dtype=np.int64) // n).astype(np.int32)[None, :]
-    return Plan(rows, tables, np.zeros(len(rows), np.int32), rw, "adjoint", row_group)
+    return Plan(rows, _adjoint_key_tables(num_angles, n), np.zeros(len(rows), np.int32), rw,
+                "adjoint", row_group)
 
 
 def adjoint_tile_height(n: int, rows_per_warp: int, warps: int, row_group: int = 1) -> int:
