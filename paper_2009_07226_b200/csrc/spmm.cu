@@ -896,7 +896,8 @@ int launch_grouped_b(const Params& p, int npl, int G, int64_t n_chunks, int thre
   if (npl == 1 && G == 4) return launch_grouped<PREC, 1, 4, CONTRACT, BULK>(p, n_chunks, threads, smem, s);
   if (npl == 2 && G == 2) return launch_grouped<PREC, 2, 2, CONTRACT, BULK>(p, n_chunks, threads, smem, s);
   if (npl == 2 && G == 4) return launch_grouped<PREC, 2, 4, CONTRACT, BULK>(p, n_chunks, threads, smem, s);
-  return xct::fail(XCT_EINVAL, "spmm: grouped rows need G in {2, 4} and 1 or 2 pieces per lane");
+  if (npl == 4 && G == 2) return launch_grouped<PREC, 4, 2, CONTRACT, BULK>(p, n_chunks, threads, smem, s);
+  return xct::fail(XCT_EINVAL, "spmm: grouped rows need G in {2, 4} and 1 or 2 pieces per lane (4 with G 2)");
 }
 
 // The register ring is the default; XCT_SPMM_BULK=1 selects the bulk-copy

@@ -458,8 +458,10 @@ class NativeDomainBuild:
         from . import pipeline
         self.g, self.cfg, self.rank, self.world, self.dev = geometry, config, rank, world, dev
         self.sa = pipeline.StreamedAssembly(geometry, config)
-        self.G = config.row_group_effective
-        self.rw = pipeline._rows_per_warp(config)
+        self.G = pipeline._side_group(config, "forward")
+        self.G_a = pipeline._side_group(config, "adjoint")
+        self.rw = pipeline._rows_per_warp(config, kind="forward")
+        self.rw_a = pipeline._rows_per_warp(config, kind="adjoint")
         self.st = _lib.stream_handle(dev)
 
     def _part(self, d_ip, d_ix, d_v, n_rows, n_cols, plan, B, nk):
@@ -577,7 +579,7 @@ class NativeDomainBuild:
         ray2pos[fp_sorted] = np.arange(len(fp_sorted), dtype=np.int32)
         d_ray2pos = torch.from_numpy(ray2pos).to(dev)
         c_local = counts[torch.from_numpy(cols).to(dev)]
-        tz = matrixstore.adjoint_tile_height(n, rw, cfg.warps_per_cta, G)
+        tz = matrixstore.adjoint_tile_height(n, self.rw_a, cfg.warps_per_cta, self.G_a)
         row_nnz = np.zeros(n, np.int64)
         np.add.at(row_nnz, cols // n, h_counts[cols])
         bands, z0 = [], 0
@@ -610,8 +612,8 @@ class NativeDomainBuild:
                           rows, k0 * n, 32 * n, lo, hi, t_ip.data_ptr(), cur.data_ptr(),
                           prev.data_ptr(), t_rows.data_ptr(), t_vals.data_ptr(), self.st)
                 del optr, oi, ov
-            plan = matrixstore.adjoint_plan(g.num_angles, n, rw, cfg.warps_per_cta, z0, z1,
-                                            row_group=G)
+            plan = matrixstore.adjoint_plan(g.num_angles, n, self.rw_a, cfg.warps_per_cta, z0, z1,
+                                            row_group=self.G_a)
             cr = plan.cta_rows
             cr = np.where(cr >= 0, cm_l[np.maximum(cr, 0)], -1)
             cr = np.where(cr >= 0, cr - lo, -1)

@@ -340,11 +340,15 @@ class DomainPartitionedSystem:
                 # the single-GPU tiles (sinogram / voxel tiles, band keys),
                 # restricted to each rank's block
                 gf = matrixstore.assign_forward_regimes(
-                    matrixstore.forward_plan(g.num_angles, n, rw, config.warps_per_cta,
-                                             row_group=config.row_group_effective),
+                    matrixstore.forward_plan(g.num_angles, n,
+                                             pipeline._rows_per_warp(config, kind="forward"),
+                                             config.warps_per_cta,
+                                             row_group=pipeline._side_group(config, "forward")),
                     g.angles, n)
-                ga = matrixstore.adjoint_plan(g.num_angles, n, rw, config.warps_per_cta,
-                                                  row_group=config.row_group_effective)
+                ga = matrixstore.adjoint_plan(g.num_angles, n,
+                                              pipeline._rows_per_warp(config, kind="adjoint"),
+                                              config.warps_per_cta,
+                                              row_group=pipeline._side_group(config, "adjoint"))
             for q in range(self.world):
                 cols, rays = tomo[q].elements, sino[q].elements
                 bip, bix, bv, f_fp = column_block(ip, ix, v, R, Cn, cols)
@@ -569,7 +573,9 @@ def build_rank_blocks_streamed(g, config, tomo, sino, rank, dev, n_threads=None)
     rw = sa.rw
     n, R, Cn = g.grid_n, g.num_rays, g.num_voxels
     st = _lib.stream_handle(dev)
-    ta = matrixstore.forward_tile_height(n, rw, config.warps_per_cta, config.row_group_effective)
+    Gf, Ga, rw_a = (pipeline._side_group(config, "forward"), pipeline._side_group(config, "adjoint"),
+                    sa.rw_a)
+    ta = matrixstore.forward_tile_height(n, rw, config.warps_per_cta, Gf)
     chunks = sa._chunks(ta)
     exp = sa._exponent(chunks) if config.precision in ("half", "mixed") else 0
     schedule = config.order == "native"
@@ -591,7 +597,7 @@ def build_rank_blocks_streamed(g, config, tomo, sino, rank, dev, n_threads=None)
         bip = np.concatenate(([0], np.cumsum(cnt[keep]))).astype(np.int64)
         gplan = matrixstore.assign_forward_regimes(
             matrixstore.forward_plan(g.num_angles, n, rw, config.warps_per_cta, k0, k1,
-                                     row_group=config.row_group_effective),
+                                     row_group=Gf),
             g.angles, n)
         plan = matrixstore.restrict_plan(gplan, fp, cols)
         hf = matrixstore.build_format(bip, bix, bv, len(fp), len(cols), plan, config.precision,
@@ -605,7 +611,7 @@ def build_rank_blocks_streamed(g, config, tomo, sino, rank, dev, n_threads=None)
     rkeep = np.zeros(R, np.uint8)
     rkeep[rays] = 1
     d_rkeep = torch.from_numpy(rkeep).to(dev)
-    tz = matrixstore.adjoint_tile_height(n, rw, config.warps_per_cta, config.row_group_effective)
+    tz = matrixstore.adjoint_tile_height(n, rw_a, config.warps_per_cta, Ga)
     per = max(1, int(sa.BAND_NNZ // (1.2 * g.num_angles * n)))
     per = max(tz, per // tz * tz)
     aparts, aps = [], []
@@ -634,8 +640,8 @@ def build_rank_blocks_streamed(g, config, tomo, sino, rank, dev, n_threads=None)
             continue
         vp = (lo + nz).astype(np.int64)
         sub_ip = np.concatenate((t_ip[nz], t_ip[-1:])).astype(np.int64)   # drop empty rows
-        gplan = matrixstore.adjoint_plan(g.num_angles, n, rw, config.warps_per_cta, z0, z1,
-                                             row_group=config.row_group_effective)
+        gplan = matrixstore.adjoint_plan(g.num_angles, n, rw_a, config.warps_per_cta, z0, z1,
+                                         row_group=Ga)
         plan = matrixstore.restrict_plan(gplan, vp, rays)
         hf = matrixstore.build_format(sub_ip, t_ix, t_v, len(vp), len(rays), plan,
                                       config.precision, config.ffactor, exp,

@@ -131,10 +131,26 @@ class SystemConfig:
     def row_group_effective(self) -> int:
         """None = 4 for native single precision (measured 13-16% faster than
         one row per lane set at c2, profiles/r01_probe_*), 1 otherwise (FP16
-        storage: one row per lane is fastest)."""
+        storage: one row per lane is fastest).  The largest of the two
+        sides' row groups (side_shape)."""
         if self.row_group is not None:
             return self.row_group
         return 4 if self.order == "native" and self.precision == "single" else 1
+
+    def side_shape(self, kind: str) -> tuple:
+        """(row_group, pieces_per_lane) of one operator direction.  Native
+        single precision with both unset: A as G=2 units of one lane (each
+        lane the whole 64-byte record of 2 rays of adjacent views), A^T as
+        G=4 units of two lanes -- measured at c2: A 58.6 -> 52.4 ms, A^T
+        46.4 ms vs 50.0 ms with G=2 (profiles/r02_probe_c2_sides.txt).
+        Both shapes give 64 rows per warp."""
+        if self.row_group is not None:
+            return self.row_group, self.pieces_per_lane or 2
+        if self.order == "native" and self.precision == "single":
+            if self.pieces_per_lane is None and self.ffactor == 16:
+                return (2, 4) if kind == "forward" else (4, 2)
+            return 4, self.pieces_per_lane or 2
+        return 1, self.pieces_per_lane or 2
 
 
 @dataclass
@@ -158,10 +174,17 @@ def configure_execution(sides, config) -> None:
             matrixstore.set_execution(blk, c and config.order == "native", config.chunk_group)
 
 
-def _rows_per_warp(cfg, row_group: int | None = None) -> int:
+def _rows_per_warp(cfg, row_group: int | None = None, kind: str | None = None) -> int:
+    if kind is not None:
+        G, ppl = cfg.side_shape(kind)
+        return 32 // matrixstore.lanes_for(cfg.ffactor, cfg.precision, ppl) * G
     ppl = cfg.pieces_per_lane or 2
     G = cfg.row_group_effective if row_group is None else row_group
     return 32 // matrixstore.lanes_for(cfg.ffactor, cfg.precision, ppl) * G
+
+
+def _side_group(cfg, kind: str) -> int:
+    return cfg.side_shape(kind)[0]
 
 
 def _csr_host(matrix):
@@ -305,7 +328,7 @@ class AssembledSystem:
 
     def _plan(self, ip, ix, n_rows, n_cols, kind):
         cfg, g = self.config, self.geometry
-        rw = _rows_per_warp(cfg)
+        rw = _rows_per_warp(cfg, kind=kind)
         if kind == "forward":
             if cfg.order == "reference" or g is None:
                 return matrixstore.reference_plan(ip, ix, n_rows, n_cols, cfg.block_partitions,
@@ -313,15 +336,15 @@ class AssembledSystem:
                                                   cfg.precision, _rows_per_warp(cfg, 1),
                                                   cfg.warps_per_cta)
             plan = matrixstore.forward_plan(g.num_angles, g.grid_n, rw, cfg.warps_per_cta,
-                                            row_group=cfg.row_group_effective)
+                                            row_group=_side_group(cfg, "forward"))
             return matrixstore.assign_forward_regimes(plan, g.angles, g.grid_n)
         # adjoint: every per-voxel order keyed by ascending ray id is the
         # reference order (src/matrixstore.py:189-201 sorts entries by ray)
         if g is not None and n_rows == g.num_voxels and n_cols == g.num_rays:
             return matrixstore.adjoint_plan(g.num_angles, g.grid_n, rw, cfg.warps_per_cta,
-                                            row_group=cfg.row_group_effective)
+                                            row_group=_side_group(cfg, "adjoint"))
         return matrixstore.row_block_plan(n_rows, n_cols, rw, cfg.warps_per_cta,
-                                          row_group=cfg.row_group_effective)
+                                          row_group=_side_group(cfg, "adjoint"))
 
     def _budget(self, plan) -> int:
         return smem_budget_for(self.config, plan)
@@ -627,7 +650,8 @@ class StreamedAssembly:
     def __init__(self, geometry: ScanGeometry, config: SystemConfig):
         self.g, self.cfg = geometry, config
         self.dev = device()
-        self.rw = _rows_per_warp(config)
+        self.rw = _rows_per_warp(config, kind="forward")
+        self.rw_a = _rows_per_warp(config, kind="adjoint")
         self._pool = {}
 
     def _buf(self, name, n, dtype, pinned=False):
@@ -696,12 +720,13 @@ class StreamedAssembly:
         import torch
         cfg, g = self.cfg, self.g
         n = g.grid_n
-        ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta, cfg.row_group_effective)
+        Gf = _side_group(cfg, "forward")
+        ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta, Gf)
         parts = []
         tm = _Timer()
         for k0, k1 in self._chunks(ta):
             plan = matrixstore.forward_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, k0, k1,
-                                            row_group=cfg.row_group_effective)
+                                            row_group=Gf)
             plan = matrixstore.assign_forward_regimes(plan, g.angles, n)
             base = k0 * n
             plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - base, -1).astype(np.int32)
@@ -729,7 +754,8 @@ class StreamedAssembly:
         import torch
         cfg, g = self.cfg, self.g
         n, R = g.grid_n, g.num_rays
-        tz = matrixstore.adjoint_tile_height(n, self.rw, cfg.warps_per_cta, cfg.row_group_effective)
+        Ga = _side_group(cfg, "adjoint")
+        tz = matrixstore.adjoint_tile_height(n, self.rw_a, cfg.warps_per_cta, Ga)
         per = max(1, int(self.BAND_NNZ // (1.2 * g.num_angles * n)))
         per = max(tz, per // tz * tz)
         st = _lib.stream_handle(self.dev)
@@ -776,8 +802,8 @@ class StreamedAssembly:
             t_ip, t_ix, t_v = _transpose(bip, bix, bv, R, hi - lo, alloc=self._buf)
             del bip, bix, bv
             tm.lap("transpose")
-            plan = matrixstore.adjoint_plan(g.num_angles, n, self.rw, cfg.warps_per_cta, z0, z1,
-                                            row_group=cfg.row_group_effective)
+            plan = matrixstore.adjoint_plan(g.num_angles, n, self.rw_a, cfg.warps_per_cta, z0, z1,
+                                            row_group=Ga)
             plan.cta_rows = np.where(plan.cta_rows >= 0, plan.cta_rows - lo, -1).astype(np.int32)
             tm.lap("plan")
             hf = matrixstore.build_format(t_ip, t_ix, t_v, hi - lo, R, plan, cfg.precision,
@@ -902,7 +928,8 @@ class StreamedAssembly:
         import torch
         from .parallel import MatrixInfo
         cfg, g = self.cfg, self.g
-        ta = matrixstore.forward_tile_height(g.grid_n, self.rw, cfg.warps_per_cta, cfg.row_group_effective)
+        ta = matrixstore.forward_tile_height(g.grid_n, self.rw, cfg.warps_per_cta,
+                                             _side_group(cfg, "forward"))
         chunks = self._chunks(ta)
         exp = self._exponent(chunks) if cfg.precision in ("half", "mixed") else 0
         self.nnz = 0
