@@ -477,13 +477,30 @@ class AssembledSystem:
             total = self._replay_hierarchical(side, parts, cd, n_chunks * F)
         else:
             total = torch.zeros((side.num_outputs, n_chunks * F), dtype=cd, device=dev)
+            cols = n_chunks * F
             for q, own in enumerate(side.ownership):
-                keep = torch.zeros(side.num_outputs, dtype=torch.bool, device=dev)
-                keep[torch.as_tensor(own, device=dev)] = True
+                keep = np.zeros(side.num_outputs, dtype=bool)
+                keep[np.asarray(own)] = True
                 for s in [q] + [s for s in range(len(parts)) if s != q]:
-                    rows = torch.as_tensor(side.footprints[s], device=dev)
-                    hit = keep[rows]
-                    total[rows[hit]] += parts[s][hit]
+                    fp = np.asarray(side.footprints[s])
+                    sel = np.nonzero(keep[fp])[0]
+                    if len(sel) == 0:
+                        continue
+                    if cd == torch.float16:          # K10 moves f32/f64 rows only
+                        idx = torch.as_tensor(sel, device=dev)
+                        total[torch.as_tensor(fp[sel], device=dev)] += parts[s][idx]
+                        continue
+                    # K10: gather the rows this owner takes from rank s, add
+                    # them at their output positions (owner first, then the
+                    # senders ascending: the direct plan's order)
+                    f64 = int(cd == torch.float64)
+                    d_sel = torch.as_tensor(sel.astype(np.int32), device=dev)
+                    d_pos = torch.as_tensor(fp[sel].astype(np.int32), device=dev)
+                    buf = torch.empty((len(sel), cols), dtype=cd, device=dev)
+                    _lib.call("xct_gather_rows", parts[s].data_ptr(), parts[s].shape[0],
+                              d_sel.data_ptr(), len(sel), 1, cols, f64, buf.data_ptr(), st)
+                    _lib.call("xct_accumulate_rows", total.data_ptr(), side.num_outputs,
+                              buf.data_ptr(), d_pos.data_ptr(), len(sel), 1, cols, f64, st)
         odt = torch.float64 if cfg.precision == "double" else torch.float32
         f_cols = fac.to(odt).repeat_interleave(F)[None, :]
         res = total.to(odt) * f_cols
