@@ -209,6 +209,21 @@ def _staging(device):
     return _stage[key]
 
 
+def host_array(shape, dtype) -> np.ndarray:
+    """A fresh host result array.  Large ones are anonymous mappings advised
+    MADV_HUGEPAGE: filling a fresh 4 KiB-page array faults every page (17.7
+    GB/s through the pinned staging on the B200 box), 2 MiB pages double it
+    (34 GB/s, tools/d2h_hugepage_probe.py)."""
+    import mmap
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape)) * dt.itemsize
+    if n < (64 << 20) or not hasattr(mmap, "MADV_HUGEPAGE"):
+        return np.empty(shape, dt)
+    m = mmap.mmap(-1, n, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    m.madvise(mmap.MADV_HUGEPAGE)
+    return np.frombuffer(m, dtype=dt).reshape(shape)
+
+
 def to_host(t, out: np.ndarray | None = None) -> np.ndarray:
     """Device tensor -> numpy array (new, or the contiguous ``out`` of the
     same byte size), via double-buffered pinned staging (pageable ``.cpu()``

@@ -486,7 +486,7 @@ class CGLSRun:
                 # and copy it through pinned staging into the result (a
                 # whole float64 x on the device would cost C*S*8 bytes)
                 torch.cuda.synchronize(cg.dev)
-                out = np.empty((n_cols, S), np.float64)
+                out = _lib.host_array((n_cols, S), np.float64)
                 per = max(1, _ROW_BLOCK_BYTES // max(1, S * 8))
                 xf = torch.empty((min(per, n_cols), S), dtype=torch.float64, device=cg.dev)
                 for r0 in range(0, n_cols, per):
