@@ -320,6 +320,12 @@ int xct_dot(const void* d_a, const void* d_b, int dtype, int64_t n_elem,
  * d_dot_partials) -> d_result[0] */
 int xct_sum_f64(const double* d_v, int64_t n, double* d_result, void* stream);
 
+/* d_hist[e] += number of positive values of d_v[0..n) with biased f64
+ * exponent e (2048 bins, caller zeroes): the binade histogram behind
+ * matrixstore.half_rescale_exponent (src/matrixstore.py:264-275) for a
+ * matrix streamed chunk by chunk */
+int xct_binade_hist(const double* d_v, int64_t n, uint64_t* d_hist, void* stream);
+
 /* max |load(v)| over n_elem -> d_maxbits[0] (IEEE bits of the f64 value,
  * atomicMax; caller zeroes it first) */
 int xct_maxabs(const void* d_v, int dtype, int64_t n_elem, float fv,

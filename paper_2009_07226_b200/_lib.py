@@ -92,6 +92,7 @@ _SIGS = {
     "xct_rows_to_chunked": (i32, [vp, i32, i64, i64, i64, i64, i32, i32, i32, vp, vp, vp, vp,
                                   vp, vp]),
     "xct_unchunk_rows_f64": (i32, [vp, i32, f32, i64, i64, i64, i64, i32, i32, vp, vp]),
+    "xct_binade_hist": (i32, [vp, i64, vp, vp]),
     "xct_gather_rows": (i32, [vp, i64, vp, i64, i64, i32, i32, vp, vp]),
     "xct_accumulate_rows": (i32, [vp, i64, vp, vp, i64, i64, i32, i32, vp]),
     "xct_scale_chunks": (i32, [vp, i64, i64, vp, i32, vp, vp, vp]),

@@ -916,3 +916,35 @@ extern "C" int xct_ipc_free(void* d_ptr) {
   if (e != cudaSuccess) return xct::fail(XCT_ECUDA, std::string("ipc_free: ") + cudaGetErrorString(e));
   return XCT_OK;
 }
+
+// ---- binade histogram (matrixstore.half_rescale_exponent, src/matrixstore.py:264-275)
+// d_hist[e] += count of positive f64 values with biased exponent e (2048
+// bins); the median's binade without sorting 1e10 lengths.  Shared-memory
+// bins per CTA, one global atomic per non-empty bin.
+namespace {
+__global__ void binade_hist_k(const double* __restrict__ v, int64_t n,
+                              unsigned long long* __restrict__ hist) {
+  __shared__ unsigned int h[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) h[i] = 0u;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = v[i];
+    if (x > 0.0) atomicAdd(&h[(unsigned)(__double_as_longlong(x) >> 52) & 2047u], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+}
+}  // namespace
+
+extern "C" int xct_binade_hist(const double* d_v, int64_t n, uint64_t* d_hist, void* stream) {
+  if (n < 0 || (n > 0 && (!d_v || !d_hist))) return xct::fail(XCT_EINVAL, "binade_hist: bad argument");
+  if (n == 0) return XCT_OK;
+  // per-CTA counts stay < 2^32: at most 148*8 CTAs, n / CTAs values each
+  const int64_t blocks = std::min<int64_t>(148 * 8, (n + 255) / 256);
+  binade_hist_k<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      d_v, n, (unsigned long long*)d_hist);
+  XCT_CUDA_CHECK_LAUNCH("binade_hist");
+  return XCT_OK;
+}

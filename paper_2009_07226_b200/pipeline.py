@@ -707,10 +707,10 @@ class StreamedAssembly:
         values when they straddle a binade (numpy median: their mean)."""
         import torch
         hist = torch.zeros(2048, dtype=torch.int64, device=self.dev)
+        st = _lib.stream_handle(self.dev)
         for k0, k1 in chunks:
             _, _, v = self._siddon(k0, k1)
-            pos = v[v > 0]
-            hist += torch.bincount((pos.view(torch.int64) >> 52), minlength=2048)
+            _lib.call("xct_binade_hist", v.data_ptr(), v.numel(), hist.data_ptr(), st)
         n = int(hist.sum())
         if n == 0:
             return 0

@@ -117,3 +117,27 @@ def test_exchange_kernels_match_indexing(f64):
               scratch.data_ptr(), ss.data_ptr(), st)
     assert torch.equal(dst, want)
     assert abs(float(ss) - float((want.double() ** 2).sum())) <= 1e-9 * float(ss)
+
+
+def test_streamed_rescale_exponent_matches_the_median():
+    """The streamed build's FP16 rescale exponent (xct_binade_hist per Siddon
+    chunk, then the median's binade) equals half_rescale_exponent over the
+    whole matrix (src/matrixstore.py:264-275), and the histogram equals
+    numpy's."""
+    from paper_2009_07226_b200 import matrixstore
+    g = geometry.make_geometry(96, 4, 64)
+    A = geometry.build_system_matrix(g)
+    _, _, v = A.host_csr32()
+    sa = pipeline.StreamedAssembly(g, pipeline.SystemConfig(precision="mixed", ffactor=16))
+    sa.CHUNK_NNZ = 5e4                                  # several chunks
+    chunks = sa._chunks(16)
+    assert len(chunks) > 1
+    assert sa._exponent(chunks) == matrixstore.half_rescale_exponent(np.asarray(v))
+    dev = geometry.device()
+    hist = torch.zeros(2048, dtype=torch.int64, device=dev)
+    d_v = torch.from_numpy(np.asarray(v)).to(dev)
+    _lib.call("xct_binade_hist", d_v.data_ptr(), d_v.numel(), hist.data_ptr(),
+              _lib.stream_handle(dev))
+    pos = np.asarray(v)[np.asarray(v) > 0]
+    want = np.bincount(pos.view(np.int64) >> 52, minlength=2048)
+    assert np.array_equal(hist.cpu().numpy(), want)
