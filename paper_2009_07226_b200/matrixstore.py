@@ -232,18 +232,21 @@ def forward_plan(num_angles: int, n: int, rows_per_warp: int, warps: int,
         ai = (w * gv + gi // gd).reshape(-1)
         di = (u * gd + gi % gd).reshape(-1)
     else:
-        td = min(_roundup(n, rw), max(rw, 32))
+        td = _forward_tile_width(n, rw)
         rpc = max(td, (rw * warps) // td * td)
         ta = rpc // td
         n_ta, n_td = -(-(k1 - k0) // ta), -(-n // td)
         cells = pseudo_hilbert_cells(n_td, n_ta)           # (x = det tile, z = view tile)
         ai, di = np.divmod(np.arange(rpc), td)
-        if _paired_setting() == "all" and td == 32 and rw == 32 and ta % 2 == 0:
+        if _paired_setting() == "all" and td in (16, 32) and rw == 32 and ta % 2 == 0:
             # view-paired lanes: warp = 2 views x 16 detectors, lanes (2k, 2k+1)
             # = one detector in adjacent views (rays that share most voxels;
             # the paired half-warp schedule merges their LDS reads)
             w, ln = np.divmod(np.arange(rpc), 32)
-            ai, di = 2 * (w // 2) + (ln & 1), 16 * (w % 2) + ln // 2
+            if td == 32:
+                ai, di = 2 * (w // 2) + (ln & 1), 16 * (w % 2) + ln // 2
+            else:
+                ai, di = 2 * w + (ln & 1), ln // 2
     k = k0 + cells[:, 1:2] * ta + ai[None, :]
     c = cells[:, 0:1] * td + di[None, :]
     rows = np.where((k < k1) & (c < n), k * n + c, -1).astype(np.int32)
@@ -268,11 +271,21 @@ def _adjoint_key_tables(num_angles: int, n: int) -> np.ndarray:
     return t
 
 
+def _forward_tile_width(n: int, rw: int) -> int:
+    """Detectors per forward CTA tile (one row per lane set): 16, i.e. tiles
+    of 16 detectors x 32 views (a warp = 2 views x 16 detectors).  Measured
+    at c5 (tools/spmm_probe.py): 32 x 16 952.6 ms, 16 x 32 937.3 ms (7.8 %
+    fewer staged records per entry, 8 % fewer load groups), 8 x 64 1056 ms.
+    XCT_FWD_TILE_DET overrides."""
+    td = int(os.environ.get("XCT_FWD_TILE_DET", "16"))
+    return min(_roundup(n, min(rw, td)), max(min(rw, td), td))
+
+
 def forward_tile_height(n: int, rows_per_warp: int, warps: int, row_group: int = 1) -> int:
     if row_group > 1:
         return warps * _unit_shape("forward", row_group)[0]
     rw = rows_per_warp
-    td = min(_roundup(n, rw), max(rw, 32))
+    td = _forward_tile_width(n, rw)
     return max(td, (rw * warps) // td * td) // td
 
 

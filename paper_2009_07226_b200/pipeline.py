@@ -958,6 +958,10 @@ class StreamedAssembly:
             try:
                 fwd = self._forward_device(exp, self.col_counts)
                 adj = self._adjoint_device(exp, chunks, self.col_counts)
+                # hand the build's cached blocks (fill scratch, band buffers)
+                # back, so the solver's large vectors do not meet a
+                # fragmented cache next to a 93 GB operator
+                torch.cuda.empty_cache()
                 info = MatrixInfo(g.num_rays, g.num_voxels, self.nnz, g.num_angles,
                                   g.num_detector_cols)
                 return self._attach(AssembledSystem.from_sides(info, cfg, g, fwd, adj, exp))

@@ -63,7 +63,7 @@ def main():
     for name, side in (("forward", system.forward), ("adjoint", system.adjoint)):
         blk = side.blocks[0]
         n_chunks = -(-S // args.ffactor)
-        x = (torch.rand((n_chunks, blk.n_in, blk.f_dev), device=dev) * 0.5).to(sd)
+        x = torch.rand((n_chunks, blk.n_in, blk.f_dev), device=dev, dtype=sd) * 0.5
         y = torch.empty((n_chunks, blk.n_out, blk.f_dev), dtype=od, device=dev)
         fac = torch.ones(n_chunks, dtype=torch.float64, device=dev)
         contracts = {"auto": [blk.contract], "0": [False], "1": [True],
@@ -104,6 +104,8 @@ def main():
                      "n_cta": int(blk.info.n_cta), "n_groups": int(blk.info.n_groups),
                      "rows_per_cta": int(blk.info.rows_per_cta),
                      "smem_bytes": blk.smem_bytes}
+        del x, y, ref_y
+        torch.cuda.empty_cache()
     print(json.dumps(out, indent=1))
 
 
