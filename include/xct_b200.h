@@ -187,7 +187,9 @@ typedef struct {
                                   fit per quarter elsewhere; d_qstats[2..3]
                                   = merged / scheduled half-warp steps,
                                   [4..5] = conflicting placements on the
-                                  per-quarter / merged steps             */
+                                  per-quarter / merged steps, [6] = half-
+                                  warps that fell back to the quarter
+                                  schedule                               */
 } xct_fmtd_part;
 
 int64_t xct_fmtd_scratch_bytes(void);

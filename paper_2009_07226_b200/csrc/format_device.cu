@@ -981,7 +981,7 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
     if ((p.fast & 0xff) >= 3)
       for (int i = 0; i < 4096; ++i) P.where[i] = -1;   // kept -1 between half jobs
   }
-  int64_t merged = 0, half_steps = 0, uconf = 0, mconf = 0;
+  int64_t merged = 0, half_steps = 0, uconf = 0, mconf = 0, fallbacks = 0;
   const double scale = ldexp(1.0, a.scale_exp);
   const bool sched = p.rq > 1;
   const int rq = sched ? p.rq : 1;
@@ -1035,6 +1035,7 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
           half_steps += width;
           continue;
         }
+        ++fallbacks;
         for (int q = 2 * h; q < 2 * h + 2; ++q) {
           bool ok = true;
           if (width <= 64)
@@ -1215,6 +1216,7 @@ __global__ void __launch_bounds__(kFillThreads) fmtd_fill_k(FillArgs a) {
     atomicAdd(&a.qstats[3], (unsigned long long)half_steps);
     atomicAdd(&a.qstats[4], (unsigned long long)uconf);
     atomicAdd(&a.qstats[5], (unsigned long long)mconf);
+    atomicAdd(&a.qstats[6], (unsigned long long)fallbacks);
   }
 }
 

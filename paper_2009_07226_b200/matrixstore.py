@@ -799,7 +799,7 @@ def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int,
     # per call (the caching allocator hands the block back to later builds
     # and, after assembly, to the solver's vectors)
     scratch = torch.empty(int(L.xct_fmtd_scratch_bytes()), dtype=torch.uint8, device=dev)
-    qs = torch.zeros(6, dtype=i64, device=dev)
+    qs = torch.zeros(7, dtype=i64, device=dev)
     d_base = torch.from_numpy(base).to(dev)
     _lib.check(L.xct_fmtd_fill(C.byref(part), lo.data_ptr(), hi.data_ptr(), bm_words,
                                widths.data_ptr(), d_base.data_ptr(), _lib.PREC_CODE[precision],
@@ -823,6 +823,7 @@ def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int,
     if q[3]:
         info["paired_merged_steps"], info["paired_half_steps"] = int(q[2]), int(q[3])
         info["paired_conflicts"] = {"quarter_steps": int(q[4]), "merged_steps": int(q[5])}
+        info["paired_fallback_halves"] = int(q[6])
     return DevicePart(T, info, rows.reshape(-1), plan.kind)
 
 
