@@ -330,7 +330,7 @@ def adjoint_plan(num_angles: int, n: int, rows_per_warp: int, warps: int,
         zi = (w * gz + gi // gx).reshape(-1)
         xi = (u * gx + gi % gx).reshape(-1)
     else:
-        tx = min(_roundup(n, rw), max(rw, 16))
+        tx = _adjoint_tile_width(n, rw)
         rpc = max(tx, (rw * warps) // tx * tx)
         tz = rpc // tx
         n_tz, n_tx = -(-(z1 - z0) // tz), -(-n // tx)
@@ -343,11 +343,21 @@ def adjoint_plan(num_angles: int, n: int, rows_per_warp: int, warps: int,
                 "adjoint", row_group)
 
 
+def _adjoint_tile_width(n: int, rw: int) -> int:
+    """Voxels along x per back-projection CTA tile (one row per lane set):
+    16, i.e. tiles of 16 x 32 voxels (a warp = 2 image rows x 16 voxels).
+    Measured at c5 (tools/spmm_probe.py): 32 x 16 825 ms, 16 x 32 811 ms
+    (same footprint, padding 1.095 -> 1.088), 64 x 8 946 ms.
+    XCT_ADJ_TILE_X overrides."""
+    tx = int(os.environ.get("XCT_ADJ_TILE_X", "16"))
+    return min(_roundup(n, min(rw, tx)), max(min(rw, tx), tx))
+
+
 def adjoint_tile_height(n: int, rows_per_warp: int, warps: int, row_group: int = 1) -> int:
     if row_group > 1:
         return warps * _unit_shape("adjoint", row_group)[0]
     rw = rows_per_warp
-    tx = min(_roundup(n, rw), max(rw, 16))
+    tx = _adjoint_tile_width(n, rw)
     return max(tx, (rw * warps) // tx * tx) // tx
 
 

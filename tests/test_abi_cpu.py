@@ -175,6 +175,11 @@ def test_bank_conflict_free_schedule(prec, side, compress, monkeypatch):
     width and tolerates a few conflicts (< 10% of quarter-steps) instead of
     extra steps."""
     monkeypatch.setenv("XCT_SCHED_COMPRESS", "1" if compress else "0")
+    # the scheduler's quality bound is stated for warps of one image row /
+    # one view (32-wide tiles); the 16-wide default tiles of the device
+    # path put two rows in a warp (16.7 % conflicting quarter-steps here)
+    monkeypatch.setenv("XCT_ADJ_TILE_X", "32")
+    monkeypatch.setenv("XCT_FWD_TILE_DET", "32")
     g = O.make_geom(40, 1, 32)
     A = O.system_matrix(g)
     ip, ix, v = A.indptr, A.indices.astype(np.int32), A.values
