@@ -361,3 +361,34 @@ def test_format_builder_random_matrices(seed, monkeypatch):
     for r in range(n_rows):
         want = sorted((int(c), float(sd(x))) for c, x in zip(ix[ip[r]:ip[r + 1]], v[ip[r]:ip[r + 1]]))
         assert sorted(seqs[r]) == want, (seed, r)
+
+
+@pytest.mark.parametrize("td,paired", [("32", "0"), ("16", "0"), ("16", "all"), ("32", "all"),
+                                       ("8", "0")])
+@pytest.mark.parametrize("tx", ["32", "16"])
+def test_tile_shapes_cover_every_row_once(td, paired, tx, monkeypatch):
+    """Forward tiles (XCT_FWD_TILE_DET, view-paired lanes) and back-projection
+    tiles (XCT_ADJ_TILE_X) are row permutations: every ray / voxel exactly
+    once, tile heights consistent with the plans; view-paired lanes hold
+    one detector in two adjacent views."""
+    from paper_2009_07226_b200 import matrixstore
+    monkeypatch.setenv("XCT_FWD_TILE_DET", td)
+    monkeypatch.setenv("XCT_ADJ_TILE_X", tx)
+    monkeypatch.setenv("XCT_FMTD_PAIRED", paired)
+    K, n, rw, warps = 100, 72, 32, 16
+    fp = matrixstore.forward_plan(K, n, rw, warps)
+    rows = fp.cta_rows[fp.cta_rows >= 0]
+    assert np.array_equal(np.sort(rows), np.arange(K * n))
+    ta = matrixstore.forward_tile_height(n, rw, warps)
+    assert ta * matrixstore._forward_tile_width(n, rw) == fp.cta_rows.shape[1]
+    if paired == "all":
+        lanes = fp.cta_rows[0].reshape(-1, 32)
+        k, c = np.divmod(lanes, n)
+        ok = lanes >= 0
+        pair_ok = (k[:, 1::2] == k[:, 0::2] + 1) & (c[:, 1::2] == c[:, 0::2])
+        assert pair_ok[ok[:, 1::2] & ok[:, 0::2]].all()
+    ap = matrixstore.adjoint_plan(K, n, rw, warps)
+    vox = ap.cta_rows[ap.cta_rows >= 0]
+    assert np.array_equal(np.sort(vox), np.arange(n * n))
+    tz = matrixstore.adjoint_tile_height(n, rw, warps)
+    assert tz * matrixstore._adjoint_tile_width(n, rw) == ap.cta_rows.shape[1]
