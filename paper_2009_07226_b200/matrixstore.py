@@ -224,13 +224,14 @@ def forward_plan(num_angles: int, n: int, rows_per_warp: int, warps: int,
     if row_group > 1:
         gv, gd = _unit_shape("forward", row_group)
         upw = rw // row_group
-        td, ta = upw * gd, warps * gv
+        ud, uv = _grouped_forward_split(upw)          # units per warp: detectors x views
+        td, ta = ud * gd, warps * uv * gv
         n_ta, n_td = -(-(k1 - k0) // ta), -(-n // td)
         cells = pseudo_hilbert_cells(n_td, n_ta)
         w, u, gi = np.meshgrid(np.arange(warps), np.arange(upw), np.arange(row_group),
                                indexing="ij")
-        ai = (w * gv + gi // gd).reshape(-1)
-        di = (u * gd + gi % gd).reshape(-1)
+        ai = ((w * uv + u // ud) * gv + gi // gd).reshape(-1)
+        di = ((u % ud) * gd + gi % gd).reshape(-1)
     else:
         td = _forward_tile_width(n, rw)
         rpc = max(td, (rw * warps) // td * td)
@@ -281,9 +282,20 @@ def _forward_tile_width(n: int, rw: int) -> int:
     return min(_roundup(n, min(rw, td)), max(min(rw, td), td))
 
 
+def _grouped_forward_split(upw: int) -> tuple:
+    """A warp's units of grouped forward rows as (along detectors, along
+    views): all along detectors unless XCT_FWD_GROUP_UD sets fewer."""
+    ud = int(os.environ.get("XCT_FWD_GROUP_UD", "0")) or upw
+    ud = max(1, min(upw, ud))
+    while upw % ud:
+        ud -= 1
+    return ud, upw // ud
+
+
 def forward_tile_height(n: int, rows_per_warp: int, warps: int, row_group: int = 1) -> int:
     if row_group > 1:
-        return warps * _unit_shape("forward", row_group)[0]
+        ud, uv = _grouped_forward_split(rows_per_warp // row_group)
+        return warps * uv * _unit_shape("forward", row_group)[0]
     rw = rows_per_warp
     td = _forward_tile_width(n, rw)
     return max(td, (rw * warps) // td * td) // td
