@@ -506,7 +506,7 @@ class NativeDomainBuild:
         n, R, Cn = g.grid_n, g.num_rays, g.num_voxels
         sa = self.sa
         G, rw = self.G, self.rw
-        ta = matrixstore.forward_tile_height(n, rw, cfg.warps_per_cta, G)
+        ta = matrixstore.forward_tile_height(n, rw, cfg.warps_per_cta, G, g.num_angles)
         chunks = sa._chunks(ta)
         exp = sa._exponent(chunks) if cfg.precision in ("half", "mixed") else 0
         self.exp = exp

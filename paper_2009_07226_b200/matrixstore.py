@@ -233,7 +233,7 @@ def forward_plan(num_angles: int, n: int, rows_per_warp: int, warps: int,
         ai = ((w * uv + u // ud) * gv + gi // gd).reshape(-1)
         di = ((u % ud) * gd + gi % gd).reshape(-1)
     else:
-        td = _forward_tile_width(n, rw)
+        td = _forward_tile_width(n, rw, num_angles)
         rpc = max(td, (rw * warps) // td * td)
         ta = rpc // td
         n_ta, n_td = -(-(k1 - k0) // ta), -(-n // td)
@@ -272,13 +272,17 @@ def _adjoint_key_tables(num_angles: int, n: int) -> np.ndarray:
     return t
 
 
-def _forward_tile_width(n: int, rw: int) -> int:
+def _forward_tile_width(n: int, rw: int, num_angles: int | None = None) -> int:
     """Detectors per forward CTA tile (one row per lane set): 16, i.e. tiles
     of 16 detectors x 32 views (a warp = 2 views x 16 detectors).  Measured
     at c5 (tools/spmm_probe.py): 32 x 16 952.6 ms, 16 x 32 937.3 ms (7.8 %
     fewer staged records per entry, 8 % fewer load groups), 8 x 64 1056 ms.
-    XCT_FWD_TILE_DET overrides."""
-    td = int(os.environ.get("XCT_FWD_TILE_DET", "16"))
+    XCT_FWD_TILE_DET overrides.  Fewer views than detectors (a tile's 32
+    views then fan out by more than 32 x pi/N) keep 32 x 16: the wider
+    footprint of 16 x 32 would exceed the device builder's 256 load groups
+    per tile (measured at 2048^2 x 512 views)."""
+    default = "16" if num_angles is None or num_angles >= n else "32"
+    td = int(os.environ.get("XCT_FWD_TILE_DET", default))
     return min(_roundup(n, min(rw, td)), max(min(rw, td), td))
 
 
@@ -292,12 +296,13 @@ def _grouped_forward_split(upw: int) -> tuple:
     return ud, upw // ud
 
 
-def forward_tile_height(n: int, rows_per_warp: int, warps: int, row_group: int = 1) -> int:
+def forward_tile_height(n: int, rows_per_warp: int, warps: int, row_group: int = 1,
+                        num_angles: int | None = None) -> int:
     if row_group > 1:
         ud, uv = _grouped_forward_split(rows_per_warp // row_group)
         return warps * uv * _unit_shape("forward", row_group)[0]
     rw = rows_per_warp
-    td = _forward_tile_width(n, rw)
+    td = _forward_tile_width(n, rw, num_angles)
     return max(td, (rw * warps) // td * td) // td
 
 

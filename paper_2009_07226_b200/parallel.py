@@ -575,7 +575,7 @@ def build_rank_blocks_streamed(g, config, tomo, sino, rank, dev, n_threads=None)
     st = _lib.stream_handle(dev)
     Gf, Ga, rw_a = (pipeline._side_group(config, "forward"), pipeline._side_group(config, "adjoint"),
                     sa.rw_a)
-    ta = matrixstore.forward_tile_height(n, rw, config.warps_per_cta, Gf)
+    ta = matrixstore.forward_tile_height(n, rw, config.warps_per_cta, Gf, g.num_angles)
     chunks = sa._chunks(ta)
     exp = sa._exponent(chunks) if config.precision in ("half", "mixed") else 0
     schedule = config.order == "native"

@@ -738,7 +738,7 @@ class StreamedAssembly:
         cfg, g = self.cfg, self.g
         n = g.grid_n
         Gf = _side_group(cfg, "forward")
-        ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta, Gf)
+        ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta, Gf, g.num_angles)
         parts = []
         tm = _Timer()
         for k0, k1 in self._chunks(ta):
@@ -849,7 +849,7 @@ class StreamedAssembly:
         import torch
         cfg, g = self.cfg, self.g
         n = g.grid_n
-        ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta, 1)
+        ta = matrixstore.forward_tile_height(n, self.rw, cfg.warps_per_cta, 1, g.num_angles)
         st = _lib.stream_handle(self.dev)
         parts = []
         tm = _Timer()
@@ -946,7 +946,7 @@ class StreamedAssembly:
         from .parallel import MatrixInfo
         cfg, g = self.cfg, self.g
         ta = matrixstore.forward_tile_height(g.grid_n, self.rw, cfg.warps_per_cta,
-                                             _side_group(cfg, "forward"))
+                                             _side_group(cfg, "forward"), g.num_angles)
         chunks = self._chunks(ta)
         exp = self._exponent(chunks) if cfg.precision in ("half", "mixed") else 0
         self.nnz = 0

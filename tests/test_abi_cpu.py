@@ -379,8 +379,8 @@ def test_tile_shapes_cover_every_row_once(td, paired, tx, monkeypatch):
     fp = matrixstore.forward_plan(K, n, rw, warps)
     rows = fp.cta_rows[fp.cta_rows >= 0]
     assert np.array_equal(np.sort(rows), np.arange(K * n))
-    ta = matrixstore.forward_tile_height(n, rw, warps)
-    assert ta * matrixstore._forward_tile_width(n, rw) == fp.cta_rows.shape[1]
+    ta = matrixstore.forward_tile_height(n, rw, warps, 1, K)
+    assert ta * matrixstore._forward_tile_width(n, rw, K) == fp.cta_rows.shape[1]
     if paired == "all":
         lanes = fp.cta_rows[0].reshape(-1, 32)
         k, c = np.divmod(lanes, n)
