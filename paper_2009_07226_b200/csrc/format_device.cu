@@ -947,15 +947,24 @@ __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int 
                   P.slot[i * kPairW + e], ja[i] + P.jo[i * kPairW + e], scale, wmax, nunder);
     }
   for (int st = 0; st < W; ++st) {
+    int16_t v[16];
+    int first_q0 = -1, first_q1 = -1;     // first record read in each quarter
+#pragma unroll
     for (int i = 0; i < 16; ++i) {
-      if (at[i * W + st] >= 0) continue;
-      int src = -1;
-      if (st >= F) {                      // merged: the partner, else any pair of the half
-        src = at[(i ^ 1) * W + st];
-        for (int o = 0; o < 16 && src < 0; ++o) src = at[o * W + st];
-      } else {                            // per quarter: the quarter's first busy lane
-        for (int o = i & 8; o < (i & 8) + 8 && src < 0; ++o) src = at[o * W + st];
+      v[i] = at[i * W + st];
+      if (v[i] >= 0) {
+        if (i < 8) { if (first_q0 < 0) first_q0 = v[i]; }
+        else if (first_q1 < 0) first_q1 = v[i];
       }
+    }
+    const int first_h = first_q0 >= 0 ? first_q0 : first_q1;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (v[i] >= 0) continue;
+      // merged steps: the partner's record, else any record of the half;
+      // per-quarter steps: the quarter's first busy lane (broadcast)
+      const int src = st >= F ? (v[i ^ 1] >= 0 ? v[i ^ 1] : first_h)
+                              : (i < 8 ? first_q0 : first_q1);
       if (src > 0)
         write_entry(a, so + ((int64_t)(st >> 2) * rpw + h * 16 + i) * 4 + (st & 3), src, -1,
                     scale, wmax, nunder);
