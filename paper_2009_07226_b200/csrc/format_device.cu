@@ -771,16 +771,21 @@ __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int 
       if (key < k0) L = M + 1; else H = M;
     }
     ja[i] = L;
+    int cnt = 0;                          // register count (n[] lives in local memory)
+    int16_t* ps = P.slot + i * kPairW;
+    int16_t* pj = P.jo + i * kPairW;
+    int16_t* pt = P.stp + i * kPairW;
     for (int64_t j = L; j < hi_j; ++j) {
       int key, coord;
       key_coord(T.mode, p.indices[j], p.B, key, coord);
       if (key >= k1) break;
-      if (n[i] >= W) return false;
-      const int e = i * kPairW + n[i]++;
-      P.slot[e] = (int16_t)(bit_rank(T, T.kbase[key] + coord - T.lo[key]) - gsb);
-      P.jo[e] = (int16_t)(j - L);
-      P.stp[e] = -1;
+      if (cnt >= W) return false;
+      ps[cnt] = (int16_t)(bit_rank(T, T.kbase[key] + coord - T.lo[key]) - gsb);
+      pj[cnt] = (int16_t)(j - L);
+      pt[cnt] = -1;
+      ++cnt;
     }
+    n[i] = cnt;
   }
   // forced double steps per pair
   int F = 0;
