@@ -184,7 +184,9 @@ typedef struct {
                                   warp schedule where sched_rq == 8 (lanes
                                   2k, 2k+1 read one record at merged steps:
                                   one LDS wavefront per half-warp), first
-                                  fit per quarter elsewhere; d_qstats[2..3]
+                                  fit per quarter elsewhere (bits 8-15:
+                                  slack steps in % of F; bit 16: first-
+                                  fit colourings); d_qstats[2..3]
                                   = merged / scheduled half-warp steps,
                                   [4..5] = conflicting placements on the
                                   per-quarter / merged steps, [6] = half-

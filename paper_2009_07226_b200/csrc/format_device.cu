@@ -397,8 +397,8 @@ struct Sched {
     freeL[er[e] * 4 + c / 64] |= 1ull << (c % 64);
     freeR[ec[e] * 4 + c / 64] |= 1ull << (c % 64);
   }
-  // Colorer::add
-  __device__ bool add(int l, int r) {
+  // Colorer::add (max_path > 0: first colour free on both sides or overflow)
+  __device__ bool add(int l, int r, int max_path = 0) {
     const int e = ne++;
     er[e] = (uint8_t)l;
     ec[e] = (uint8_t)r;
@@ -406,6 +406,9 @@ struct Sched {
     const int a = first_free(freeL, l), b = first_free(freeR, r);
     if (a < 0 || b < 0) return false;
     if (atR[r * nc + a] >= 0) {
+      // greedy mode (paired schedule of A): no alternating path, the edge
+      // goes to the caller's overflow placement
+      if (max_path > 0) { col[e] = 0x7fff; return true; }
       int np = 0, v = r, want = a;
       bool right = true;
       for (;;) {
@@ -697,7 +700,7 @@ constexpr int64_t kFillScratch = Sched::bytes() + PairScr::bytes();   // per fil
 // max(ncol, class degree) colours; edges on colours >= ncol are the
 // overflow.  Returns the colour count used, -1 when it does not fit.
 __device__ int colour_core(Sched& S, int ne, int nrows, int ncol, const int16_t* ent,
-                           const int16_t* slot) {
+                           const int16_t* slot, bool greedy) {
   if (ncol < 1) return -1;
   int cnt8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int e = 0; e < ne; ++e) ++cnt8[slot[ent[e]] & 7];
@@ -706,7 +709,7 @@ __device__ int colour_core(Sched& S, int ne, int nrows, int ncol, const int16_t*
   if (maxdeg > kNcMax) return -1;
   S.reset(nrows, maxdeg);
   for (int e = 0; e < ne; ++e)
-    if (!S.add(S.eidx[e], slot[ent[e]] & 7)) return -1;
+    if (!S.add(S.eidx[e], slot[ent[e]] & 7, greedy ? 1 : 0)) return -1;
   return maxdeg;
 }
 // Overflow edges (colour >= ncol; colour -2 = moved elsewhere, skipped)
@@ -802,6 +805,7 @@ __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int 
   if (F > 0 && extra_pct) F = min(W, F + max(1, (F * extra_pct + 99) / 100));
   const int M = W - F;
   const bool minimal_u = (p.fast & 0xff) == 4;
+  const bool greedy = (p.fast >> 16) & 1;  // first-fit colourings (measured better for A)
   // per pair: which entries take the per-quarter steps [0, F) (marked -3),
   // the rest become merged-region tokens (ta: lane a entry, tb: lane b
   // entry, global indices lane * kPairW + e, -1: that lane idles)
@@ -878,7 +882,7 @@ __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int 
       P.tu[e] = P.ta[e] >= 0 ? P.ta[e] : P.tb[e];
       S.eidx[e] = (int16_t)((P.tu[e] / kPairW) >> 1);
     }
-    if (colour_core(S, nt, 8, M, P.tu, P.slot) < 0) return false;
+    if (colour_core(S, nt, 8, M, P.tu, P.slot, greedy) < 0) return false;
     for (int e = 0; e < nt; ++e) {
       if (S.col[e] < M) continue;
       const int ea = P.ta[e], eb = P.tb[e];
@@ -913,7 +917,7 @@ __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int 
           ++ne;
         }
     if (!ne) continue;
-    if (colour_core(S, ne, 8, F, P.tu, P.slot) < 0) return false;
+    if (colour_core(S, ne, 8, F, P.tu, P.slot, greedy) < 0) return false;
     // a class's overflow takes a free merged step of its pair where its
     // class is free (the partner idles there), else conflicts on [0, F)
     for (int e = 0; e < ne; ++e) {
