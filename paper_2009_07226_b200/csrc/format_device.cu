@@ -397,7 +397,9 @@ struct Sched {
     freeL[er[e] * 4 + c / 64] |= 1ull << (c % 64);
     freeR[ec[e] * 4 + c / 64] |= 1ull << (c % 64);
   }
-  // Colorer::add (max_path > 0: first colour free on both sides or overflow)
+  // Colorer::add (max_path 0: alternating paths -- the host's algorithm;
+  // max_path < 0: first fit, see below)
+  static constexpr int16_t kOverflowCol = 0x7fff;
   __device__ bool add(int l, int r, int max_path = 0) {
     const int e = ne++;
     er[e] = (uint8_t)l;
@@ -406,9 +408,9 @@ struct Sched {
     const int a = first_free(freeL, l), b = first_free(freeR, r);
     if (a < 0 || b < 0) return false;
     if (atR[r * nc + a] >= 0) {
-      // greedy mode (paired schedule of A): no alternating path, the edge
-      // goes to the caller's overflow placement
-      if (max_path > 0) { col[e] = 0x7fff; return true; }
+      // max_path < 0: no alternating path (first fit; the paired schedule
+      // of A); a refused edge goes to the caller's overflow placement
+      if (max_path < 0) { col[e] = kOverflowCol; return true; }
       int np = 0, v = r, want = a;
       bool right = true;
       for (;;) {
@@ -709,7 +711,7 @@ __device__ int colour_core(Sched& S, int ne, int nrows, int ncol, const int16_t*
   if (maxdeg > kNcMax) return -1;
   S.reset(nrows, maxdeg);
   for (int e = 0; e < ne; ++e)
-    if (!S.add(S.eidx[e], slot[ent[e]] & 7, greedy ? 1 : 0)) return -1;
+    if (!S.add(S.eidx[e], slot[ent[e]] & 7, greedy ? -1 : 0)) return -1;
   return maxdeg;
 }
 // Overflow edges (colour >= ncol; colour -2 = moved elsewhere, skipped)
@@ -805,7 +807,7 @@ __device__ bool paired_half(const FillArgs& a, const Tile& T, int64_t tile, int 
   if (F > 0 && extra_pct) F = min(W, F + max(1, (F * extra_pct + 99) / 100));
   const int M = W - F;
   const bool minimal_u = (p.fast & 0xff) == 4;
-  const bool greedy = (p.fast >> 16) & 1;  // first-fit colourings (measured better for A)
+  const bool greedy = (p.fast >> 16) & 1;  // first-fit colourings (faster fill)
   // per pair: which entries take the per-quarter steps [0, F) (marked -3),
   // the rest become merged-region tokens (ta: lane a entry, tb: lane b
   // entry, global indices lane * kPairW + e, -1: that lane idles)
