@@ -735,12 +735,13 @@ def _sched_mode(exact: bool, kind: str = "forward") -> int:
         mode = 3 if os.environ.get("XCT_FMTD_PAIRED_FILL") == "1" else 4
         extra = int(os.environ.get("XCT_FMTD_PAIRED_EXTRA", "20"))  # % of F, slack steps
         # first-fit colourings (no alternating paths): 27 % less fill time;
-        # for A also fewer modelled wavefronts, for A^T +2.6 % of them
-        # (c5: 1,793.5 -> 1,802.1 ms/iter for assembly 31.6 -> 29.4 s, the
-        # better time to solution below ~300 iterations).  XCT_FMTD_PAIRED_
-        # GREEDY=0 keeps the alternating-path colourer for A^T.
-        greedy = 0 if (kind == "adjoint" and
-                       os.environ.get("XCT_FMTD_PAIRED_GREEDY") == "0") else 1
+        # for A also fewer modelled wavefronts (used there), for A^T +2.6 %
+        # of them (c5: 1,793.5 -> 1,802.1 ms/iter for assembly 31.6 -> 29.4 s,
+        # and c1's native-order deviation from the reference 1.4e-3 ->
+        # 2.5e-3, closer to its bound): A^T keeps the alternating-path
+        # colourer unless XCT_FMTD_PAIRED_GREEDY=1
+        greedy = 1 if (kind == "forward" or
+                       os.environ.get("XCT_FMTD_PAIRED_GREEDY") == "1") else 0
         return mode | (min(max(extra, 0), 255) << 8) | (greedy << 16)
     return 1
 
