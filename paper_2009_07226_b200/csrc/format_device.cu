@@ -641,7 +641,7 @@ __device__ __noinline__ void greedy_quarter_wide(const FillArgs& a, const Tile& 
   }
 }
 
-// ---- paired half-warp schedule (sched mode 3) ------------------------------
+// ---- paired half-warp schedule (sched modes 3 and 4) ------------------------
 // A warp LDS.128 costs one shared-memory wavefront per half-warp (instead of
 // two) when each quarter of the half reads at most 4 distinct 16-byte
 // records and the half's records sit in distinct bank quads
@@ -651,12 +651,16 @@ __device__ __noinline__ void greedy_quarter_wide(const FillArgs& a, const Tile& 
 // rows touch, or one row's entry while its partner idles -- and the 8 pairs
 // read records of 8 distinct bank classes.  Per (group, warp, half):
 //   forced_k = max(0, n_a + n_b - shared_k - W) steps where pair k must read
-//   two records; F = max_k forced_k.  Steps [0, F) are scheduled per quarter
-//   as today (first fit over bank classes), pair k's doubles first; steps
-//   [F, W) are merged: the pairs' remaining tokens (shared entries and
-//   singles) are edge-coloured pairs x bank classes by the same alternating-
-//   path colourer as the quarter schedule (Sched), overflow of a class
-//   beyond W - F steps placed where it conflicts least.
+//   two records; F = max_k forced_k, raised by a slack of (sched_fast bits
+//   8-15) % for the tightest pairs.  Steps [F, W) are merged: the pairs'
+//   tokens (shared entries and singles) are edge-coloured pairs x bank
+//   classes.  Steps [0, F) are scheduled per quarter (lanes x bank classes)
+//   and take, per pair, only the entries the merged steps cannot hold (mode
+//   4; mode 3 fills them first).  A class overflowing the merged steps moves
+//   to the per-quarter steps where its lanes have room and vice versa (a
+//   free merged step of the pair whose class is free); what is left takes
+//   the least-conflict free step.  Colourings: the quarter schedule's
+//   alternating-path colourer (Sched), or first fit (sched_fast bit 16).
 // Same entries per row and slab as every other schedule (only the steps
 // differ), so sums agree to rounding (native order).  Device-only: the host
 // builder has no such mode and stays the oracle for modes 0-2.
