@@ -832,8 +832,11 @@ def build_format_device(d_indptr, d_indices, d_values, n_rows: int, n_cols: int,
                                   else torch.float32, device=dev)
         T["slots"] = torch.zeros(n_padded + extra, dtype=torch.int16, device=dev)
     # per call (the caching allocator hands the block back to later builds
-    # and, after assembly, to the solver's vectors)
-    scratch = torch.empty(int(L.xct_fmtd_scratch_bytes()), dtype=torch.uint8, device=dev)
+    # and, after assembly, to the solver's vectors); the fill runs
+    # min(n_cta, 2 x 148) CTAs, so small parts need a fraction of it
+    full = int(L.xct_fmtd_scratch_bytes())
+    ctas = min(int(n_cta), 2 * 148)
+    scratch = torch.empty(max(1, full * ctas // (2 * 148)), dtype=torch.uint8, device=dev)
     qs = torch.zeros(7, dtype=i64, device=dev)
     d_base = torch.from_numpy(base).to(dev)
     _lib.check(L.xct_fmtd_fill(C.byref(part), lo.data_ptr(), hi.data_ptr(), bm_words,
