@@ -236,7 +236,7 @@ def _half_wavefronts(part, lanes_per_row=1):
     return wf, hs
 
 
-@pytest.mark.parametrize("mode", ["min", "fill"])
+@pytest.mark.parametrize("mode", ["min", "fill", "greedy"])
 @pytest.mark.parametrize("kind", ["forward", "adjoint"])
 def test_paired_schedule_places_the_same_entries_and_merges(kind, mode, monkeypatch):
     """Sched mode 3 (paired half-warp schedule): the same groups, maps,
@@ -270,6 +270,8 @@ def test_paired_schedule_places_the_same_entries_and_merges(kind, mode, monkeypa
     monkeypatch.setenv("XCT_FMTD_PAIRED", "all")
     if mode == "fill":
         monkeypatch.setenv("XCT_FMTD_PAIRED_FILL", "1")
+    if mode == "greedy":                     # first-fit colourings on both sides
+        monkeypatch.setenv("XCT_FMTD_PAIRED_GREEDY", "1")
     paired = matrixstore.build_format_device(*args)
     T = {k2: t.cpu().numpy() for k2, t in paired.tensors.items()}
     for k2 in ("cta_group_ptr", "group_map_ptr", "group_map", "slab_off", "slab_width"):
