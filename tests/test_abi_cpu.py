@@ -392,3 +392,39 @@ def test_tile_shapes_cover_every_row_once(td, paired, tx, monkeypatch):
     assert np.array_equal(np.sort(vox), np.arange(n * n))
     tz = matrixstore.adjoint_tile_height(n, rw, warps)
     assert tz * matrixstore._adjoint_tile_width(n, rw) == ap.cta_rows.shape[1]
+
+
+def test_schedule_mode_encoding(monkeypatch):
+    """sched_fast as xct_fmtd_part documents it: low byte = mode (0 exact,
+    1 default host schedule, 2 first fit, 3/4 paired), bits 8-15 = slack %
+    of the paired schedule, bit 16 = first-fit colourings (A by default)."""
+    from paper_2009_07226_b200 import matrixstore
+    for k in ("XCT_FMTD_EXACT", "XCT_FMTD_FAST", "XCT_FMTD_PAIRED", "XCT_FMTD_PAIRED_FILL",
+              "XCT_FMTD_PAIRED_EXTRA", "XCT_FMTD_PAIRED_GREEDY"):
+        monkeypatch.delenv(k, raising=False)
+    assert matrixstore._sched_mode(True, "adjoint") == 0
+    assert matrixstore._sched_mode(False, "forward") == 1
+    assert matrixstore._sched_mode(False, "adjoint") == 4 | (20 << 8)
+    monkeypatch.setenv("XCT_FMTD_PAIRED", "all")
+    assert matrixstore._sched_mode(False, "forward") == 4 | (20 << 8) | (1 << 16)
+    monkeypatch.setenv("XCT_FMTD_PAIRED_FILL", "1")
+    monkeypatch.setenv("XCT_FMTD_PAIRED_EXTRA", "35")
+    monkeypatch.setenv("XCT_FMTD_PAIRED_GREEDY", "1")
+    assert matrixstore._sched_mode(False, "adjoint") == 3 | (35 << 8) | (1 << 16)
+    monkeypatch.setenv("XCT_FMTD_PAIRED", "0")
+    assert matrixstore._sched_mode(False, "adjoint") == 1
+    monkeypatch.setenv("XCT_FMTD_FAST", "1")
+    assert matrixstore._sched_mode(False, "adjoint") == 2
+
+
+def test_host_result_arrays():
+    """_lib.host_array: huge-page mapping for large results, plain numpy for
+    small ones; writable, C-contiguous, right shape and dtype."""
+    big = _lib.host_array((1 << 20, 16), np.float64)
+    assert big.shape == (1 << 20, 16) and big.dtype == np.float64
+    assert big.flags.writeable and big.flags.c_contiguous
+    big[-1, -1] = 3.5
+    assert big[-1, -1] == 3.5
+    small = _lib.host_array((3, 5), np.float32)
+    assert small.shape == (3, 5) and small.dtype == np.float32
+    assert _lib.host_array((0, 4), np.float64).shape == (0, 4)
