@@ -325,8 +325,10 @@ class AdjointSide:
         """Owners push their normalized inputs straight into the consumers'
         K6 input buffers over NVLink: one gather kernel per consumer whose
         destination is the consumer's buffer (CUDA IPC mapping) -- gather
-        and transfer in one pass, no NCCL staging; then K6 on the whole
-        element-major input."""
+        and transfer in one pass, no NCCL staging.  In F-chunk waves: the
+        receive buffer is wave-major ([wave][footprint][chunks of the wave]
+        [record]), wave w+1's gathers run on a side stream while K6 consumes
+        wave w, a flag all-reduce per wave marks its stores landed."""
         import torch
         import torch.distributed as dist
         C, fd = cg.n_chunks, cg.f_dev
@@ -338,42 +340,62 @@ class AdjointSide:
                 self._ipc.close()
             self._ipc = IpcBuffer(self.n_fp * C * rec, self.rank, self.world)
             self._flag = torch.zeros(1, dtype=torch.float32, device=cg.dev)
+            self._side = torch.cuda.Stream(device=cg.dev)
             self._ipc_key = key
         o = out.view(C, self.num_outputs, fd)
         blk = self.block
-        parts = torch.empty(C * blk.info.n_cta, dtype=torch.float64, device=cg.dev)
-        dist.all_reduce(self._flag)           # consumers are done with their inputs
+        n_cta = blk.info.n_cta
+        parts = torch.empty(C * n_cta, dtype=torch.float64, device=cg.dev)
         prof = os.environ.get("XCT_EXCHANGE_PROFILE") == "1"
+        waves = _Waves.bounds(C) if not prof else [(0, C)]
+        main = torch.cuda.current_stream(cg.dev)
+        side = self._side
+        dist.all_reduce(self._flag)           # consumers are done with their inputs
         if prof:
             import time
             torch.cuda.synchronize()
             t0 = time.perf_counter()
+        side.wait_stream(main)
+        st_side = int(side.cuda_stream)
+        ready = []
         a, b = self.seg[self.rank], self.seg[self.rank + 1]
-        _lib.call("xct_gather_records", xin.data_ptr(), self.num_inputs, self.self_pos.data_ptr(),
-                  b - a, 0, C, rec, self._ipc.ptr + a * C * rec if b > a else None, cg.st)
-        for q, idx in self.send_idx.items():
-            dst = self._ipc.peer[q] + self.seg_of[q][self.rank] * C * rec
-            _lib.call("xct_gather_records", xin.data_ptr(), self.num_inputs, idx.data_ptr(),
-                      idx.numel(), 0, C, rec, dst, cg.st)
-            self.stats.bytes_out += idx.numel() * C * rec
-        dist.all_reduce(self._flag)           # every producer's stores landed
+        with torch.cuda.stream(side):
+            for c0, c1 in waves:
+                cw = c1 - c0
+                base = self.n_fp * c0 * rec              # this wave's region, my buffer
+                _lib.call("xct_gather_records", xin.data_ptr(), self.num_inputs,
+                          self.self_pos.data_ptr(), b - a, c0, cw, rec,
+                          self._ipc.ptr + base + a * cw * rec if b > a else None, st_side)
+                for q, idx in self.send_idx.items():
+                    n_fp_q = self.seg_of[q][-1]
+                    dst = self._ipc.peer[q] + n_fp_q * c0 * rec + \
+                        self.seg_of[q][self.rank] * cw * rec
+                    _lib.call("xct_gather_records", xin.data_ptr(), self.num_inputs,
+                              idx.data_ptr(), idx.numel(), c0, cw, rec, dst, st_side)
+                    self.stats.bytes_out += idx.numel() * cw * rec
+                dist.all_reduce(self._flag)       # every producer's wave stores landed
+                e = torch.cuda.Event()
+                e.record(side)
+                ready.append(e)
         if prof:
             torch.cuda.synchronize()
             self.stats.seconds += time.perf_counter() - t0
-        xfp = torch.empty(0, dtype=xin.dtype, device=cg.dev)
         ev = cg.events
-        if ev is not None:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-        engine.apply_side_ptr(blk, self._ipc.ptr, C, o, row_stride=fd,
-                              chunk_stride=self.num_outputs * fd, valid_cols=C * fd,
-                              ffactor_out=fd, factors=fac, dot_partials=parts, stream=cg.st,
-                              x_chunk_stride=1, x_elem_stride=C)
-        if ev is not None:
-            e1.record()
-            ev.append((False, e0, e1, 1.0))
-        del xfp
+        for (c0, c1), e in zip(waves, ready):
+            cw = c1 - c0
+            main.wait_event(e)
+            if ev is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            engine.apply_side_ptr(blk, self._ipc.ptr + self.n_fp * c0 * rec, cw, o[c0:c1],
+                                  row_stride=fd, chunk_stride=self.num_outputs * fd,
+                                  valid_cols=cw * fd, ffactor_out=fd, factors=fac[c0:c1],
+                                  dot_partials=parts[c0 * n_cta:c1 * n_cta], stream=cg.st,
+                                  x_chunk_stride=1, x_elem_stride=cw)
+            if ev is not None:
+                e1.record()
+                ev.append((False, e0, e1, cw / C))
         self.stats.calls += 1
         _lib.call("xct_sum_f64", parts.data_ptr(), parts.numel(), cg.scal.data_ptr(), cg.st)
         return float(cg.scal[0].item())
